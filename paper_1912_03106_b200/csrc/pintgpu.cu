@@ -1,0 +1,789 @@
+// libpintgpu -- C ABI of the batched-Phi MGRIT hot path (see include/pintgpu.h).
+// Host side of the library: per-device context, level upload, workspace,
+// launch sequencing of the batched PCG / Newton and the MGRIT kernels.
+#include "pintgpu.h"
+#include "common.cuh"
+#include "pcg.cuh"
+#include "pcg_dia.cuh"
+#include "mgrit_ops.cuh"
+#include "newton.cuh"
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace {
+
+struct Level {
+    int n = 0, nnz = 0, n_src = 0, side = 0;
+    int* row_ptr = nullptr;
+    int* col_idx = nullptr;
+    double* m_val = nullptr;
+    double* k_val = nullptr;
+    double* dM = nullptr;
+    double* dK = nullptr;
+    double* shapes = nullptr;
+    double* weights = nullptr;
+    // streamed tiling
+    int R = 1024, n_tiles = 0, span_max = 0, C = 1;
+    int* tile_lo = nullptr;
+    int* tile_hi = nullptr;
+    bool resident = false;
+    // symmetric DIA layout of the streamed path (preferred when available)
+    bool dia = false;
+    int U = 0, omax = 0, ld = 0, Cd = 1;
+    int off[PG_DIA_MAX + 1] = {0};
+    double2* mk = nullptr;
+    DiaWork V{};
+    // nonlinear iron elements
+    int n_elem = 0;
+    int* elem_dof = nullptr;
+    double* elem_geo = nullptr;
+    int* ne_ptr = nullptr;
+    int* ne = nullptr;
+    // workspace
+    int ws_B = 0;
+    PcgWork W{};
+    NewtonWork NW{};
+    std::vector<void*> ws_allocs;
+};
+
+}  // namespace
+
+struct pg_ctx {
+    int device = 0;
+    int n_sm = 148;
+    std::vector<Level> levels;
+    pg_solver_opts opts{};
+    std::string err;
+    int64_t launches = 0;
+    pg_phi_stats last{};
+    pg_phi_stats total{};
+    // stats accumulators on device
+    unsigned long long* d_iters = nullptr;  // [0] cumulative, [1] this call
+    int* d_ictr = nullptr;                  // [0] max iters this call, [1] failed cumulative, [2] failed this call
+    int* h_poll = nullptr;        // pinned
+    int last_level = -1;
+    int newton_fail_col = -1, newton_fail_iters = 0;
+};
+
+static int set_err(pg_ctx* ctx, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    return code;
+}
+
+#define CU(call)                                                               \
+    do {                                                                       \
+        cudaError_t e_ = (call);                                               \
+        if (e_ != cudaSuccess)                                                 \
+            return set_err(ctx, PG_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__,  \
+                           #call, cudaGetErrorString(e_));                     \
+    } while (0)
+
+#define LAUNCHED()                                                             \
+    do {                                                                       \
+        ctx->launches++;                                                       \
+        ctx->last.launches++;                                                  \
+        cudaError_t e_ = cudaGetLastError();                                   \
+        if (e_ != cudaSuccess)                                                 \
+            return set_err(ctx, PG_ECUDA, "%s:%d launch: %s", __FILE__,        \
+                           __LINE__, cudaGetErrorString(e_));                  \
+    } while (0)
+
+template <typename T>
+static int dev_upload(pg_ctx* ctx, T** dst, const T* src, size_t count) {
+    CU(cudaMalloc((void**)dst, std::max<size_t>(count, 1) * sizeof(T)));
+    if (count) CU(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return PG_OK;
+}
+
+static PcgLevel pcg_view(const Level& L) {
+    PcgLevel v;
+    v.n = L.n;
+    v.row_ptr = L.row_ptr;
+    v.col_idx = L.col_idx;
+    v.m_val = L.m_val;
+    v.k_val = L.k_val;
+    v.dM = L.dM;
+    v.dK = L.dK;
+    v.n_src = L.n_src;
+    v.shapes = L.shapes;
+    v.R = L.R;
+    v.n_tiles = L.n_tiles;
+    v.tile_lo = L.tile_lo;
+    v.tile_hi = L.tile_hi;
+    return v;
+}
+
+static size_t stream_smem(const Level& L, int C, bool guess) {
+    return (size_t)C * L.span_max * sizeof(double) * (guess ? 2 : 1);
+}
+
+// ---------------------------------------------------------------------------
+extern "C" int pg_create(pg_ctx** out, int device) {
+    if (!out) return PG_EINVAL;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
+        return PG_ECUDA;
+    pg_ctx* ctx = new pg_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return PG_ECUDA; }
+    cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
+    ctx->opts.rtol = 1e-13;
+    ctx->opts.max_iters = 20000;
+    ctx->opts.check_every = 16;
+    ctx->opts.newton_tol = 1e-11;
+    ctx->opts.newton_max_iters = 25;
+    ctx->opts.damping = 0.5;
+    ctx->opts.max_halvings = 8;
+    ctx->opts.nu0 = 1.0;
+    ctx->opts.k1 = 0.0;
+    ctx->opts.k2 = 0.0;
+    ctx->opts.k3 = 1.0;
+    if (cudaMalloc(&ctx->d_iters, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ictr, 3 * sizeof(int)) != cudaSuccess ||
+        cudaMemset(ctx->d_iters, 0, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(ctx->d_ictr, 0, 3 * sizeof(int)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_poll, 16 * sizeof(int)) != cudaSuccess) {
+        delete ctx;
+        return PG_ECUDA;
+    }
+    *out = ctx;
+    return PG_OK;
+}
+
+static void free_level(Level& L) {
+    void* ptrs[] = {L.row_ptr, L.col_idx, L.m_val, L.k_val, L.dM, L.dK, L.shapes,
+                    L.weights, L.tile_lo, L.tile_hi, L.elem_dof, L.elem_geo,
+                    L.ne_ptr, L.ne, L.mk};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (void* p : L.ws_allocs) cudaFree(p);
+    L.ws_allocs.clear();
+}
+
+extern "C" void pg_destroy(pg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (auto& L : ctx->levels) free_level(L);
+    cudaFree(ctx->d_iters);
+    cudaFree(ctx->d_ictr);
+    cudaFreeHost(ctx->h_poll);
+    delete ctx;
+}
+
+extern "C" const char* pg_last_error(pg_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : "null context";
+}
+
+extern "C" int pg_set_options(pg_ctx* ctx, const pg_solver_opts* o) {
+    if (!ctx || !o) return PG_EINVAL;
+    if (!(o->rtol > 0.0) || o->max_iters < 1 || o->check_every < 1)
+        return set_err(ctx, PG_EINVAL, "rtol must be > 0, max_iters and check_every >= 1");
+    if (!(o->damping > 0.0 && o->damping <= 1.0))
+        return set_err(ctx, PG_EINVAL, "damping must lie in (0, 1], got %g", o->damping);
+    if (o->newton_max_iters < 1 || !(o->newton_tol > 0.0))
+        return set_err(ctx, PG_EINVAL, "newton max_iters must be >= 1 and tol positive");
+    ctx->opts = *o;
+    return PG_OK;
+}
+
+extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
+    if (!ctx || !d) return -1;
+    if (d->n < 1 || d->nnz < d->n || !d->row_ptr || !d->col_idx || !d->m_val || !d->k_val) {
+        set_err(ctx, PG_EINVAL, "level needs n >= 1 and a CSR with a diagonal");
+        return -1;
+    }
+    CU(cudaSetDevice(ctx->device));
+    Level L;
+    L.n = d->n;
+    L.nnz = d->nnz;
+    L.n_src = d->n_src;
+    L.side = d->side;
+    // diagonals, halo ranges, validation on the host
+    std::vector<double> dM(d->n, 0.0), dK(d->n, 0.0);
+    for (int i = 0; i < d->n; ++i) {
+        bool diag = false;
+        for (int e = d->row_ptr[i]; e < d->row_ptr[i + 1]; ++e) {
+            int j = d->col_idx[e];
+            if (j < 0 || j >= d->n) {
+                set_err(ctx, PG_EINVAL, "column index %d out of range in row %d", j, i);
+                return -1;
+            }
+            if (j == i) { dM[i] += d->m_val[e]; dK[i] += d->k_val[e]; diag = true; }
+        }
+        if (!diag) {
+            set_err(ctx, PG_EINVAL, "row %d has no diagonal entry", i);
+            return -1;
+        }
+    }
+    L.resident = d->n <= PG_RES_MAX;
+    // rows per tile: 1024 (4 rows per thread); halo from the CSR
+    L.R = 1024;
+    L.n_tiles = (d->n + L.R - 1) / L.R;
+    std::vector<int> lo(L.n_tiles), hi(L.n_tiles);
+    L.span_max = 0;
+    for (int t = 0; t < L.n_tiles; ++t) {
+        int r0 = t * L.R, r1 = std::min(d->n, r0 + L.R);
+        int l = r0, h = r1;
+        for (int i = r0; i < r1; ++i)
+            for (int e = d->row_ptr[i]; e < d->row_ptr[i + 1]; ++e) {
+                l = std::min(l, d->col_idx[e]);
+                h = std::max(h, d->col_idx[e] + 1);
+            }
+        lo[t] = l;
+        hi[t] = h;
+        L.span_max = std::max(L.span_max, h - l);
+    }
+    // columns per CTA: the largest C with C * span * 8 B <= 96 KB (2 CTAs/SM)
+    L.C = 8;
+    while (L.C > 1 && (size_t)L.C * L.span_max * 8 > 96 * 1024) L.C >>= 1;
+    if ((size_t)L.span_max * 8 * 2 > 200 * 1024) {
+        set_err(ctx, PG_EINVAL, "matrix bandwidth too large for the tiled kernels (span %d)",
+                L.span_max);
+        return -1;
+    }
+    // symmetric DIA detection: <= PG_DIA_MAX distinct upper offsets and
+    // M, K exactly symmetric
+    {
+        std::vector<int> offs;
+        bool ok = true;
+        for (int i = 0; i < d->n && ok; ++i)
+            for (int e = d->row_ptr[i]; e < d->row_ptr[i + 1]; ++e) {
+                int o = d->col_idx[e] - i;
+                if (o > 0 && std::find(offs.begin(), offs.end(), o) == offs.end()) {
+                    offs.push_back(o);
+                    if ((int)offs.size() > PG_DIA_MAX) { ok = false; break; }
+                }
+            }
+        std::sort(offs.begin(), offs.end());
+        if (ok) {
+            const int U = (int)offs.size();
+            std::vector<double2> mk((size_t)(U + 1) * d->n, make_double2(0.0, 0.0));
+            auto slot = [&](int o) -> int {
+                if (o == 0) return 0;
+                for (int u = 0; u < U; ++u) if (offs[u] == o) return u + 1;
+                return -1;
+            };
+            for (int i = 0; i < d->n; ++i)
+                for (int e = d->row_ptr[i]; e < d->row_ptr[i + 1]; ++e) {
+                    int o = d->col_idx[e] - i;
+                    if (o >= 0) {
+                        double2& v = mk[(size_t)slot(o) * d->n + i];
+                        v.x += d->m_val[e];
+                        v.y += d->k_val[e];
+                    }
+                }
+            // symmetry check: lower entries must mirror the stored upper ones
+            std::vector<double2> lowsum((size_t)(U + 1) * d->n, make_double2(0.0, 0.0));
+            for (int i = 0; i < d->n && ok; ++i)
+                for (int e = d->row_ptr[i]; e < d->row_ptr[i + 1]; ++e) {
+                    int o = i - d->col_idx[e];
+                    if (o > 0) {
+                        int u = slot(o);
+                        if (u < 0) { ok = false; break; }
+                        double2& v = lowsum[(size_t)u * d->n + d->col_idx[e]];
+                        v.x += d->m_val[e];
+                        v.y += d->k_val[e];
+                    }
+                }
+            for (size_t k = (size_t)d->n; ok && k < mk.size(); ++k)
+                if (mk[k].x != lowsum[k].x || mk[k].y != lowsum[k].y) ok = false;
+            if (ok) {
+                L.dia = true;
+                L.U = U;
+                L.omax = U ? offs[U - 1] : 0;
+                for (int u = 0; u < U; ++u) L.off[u + 1] = offs[u];
+                L.ld = (d->n + 31) & ~31;
+                const int span = L.R + 2 * L.omax + 4;
+                L.Cd = 4;
+                while (L.Cd > 1 && (size_t)L.Cd * span * 8 > 72 * 1024) L.Cd >>= 1;
+                if ((size_t)span * 8 > 200 * 1024 || U == 0) L.dia = false;
+                if (L.dia) {
+                    int rc0 = dev_upload(ctx, &L.mk, mk.data(), mk.size());
+                    if (rc0) return -1;
+                }
+            }
+        }
+    }
+    int rc;
+    if ((rc = dev_upload(ctx, &L.row_ptr, d->row_ptr, (size_t)d->n + 1)) ||
+        (rc = dev_upload(ctx, &L.col_idx, d->col_idx, (size_t)d->nnz)) ||
+        (rc = dev_upload(ctx, &L.m_val, d->m_val, (size_t)d->nnz)) ||
+        (rc = dev_upload(ctx, &L.k_val, d->k_val, (size_t)d->nnz)) ||
+        (rc = dev_upload(ctx, &L.dM, dM.data(), dM.size())) ||
+        (rc = dev_upload(ctx, &L.dK, dK.data(), dK.size())) ||
+        (rc = dev_upload(ctx, &L.tile_lo, lo.data(), lo.size())) ||
+        (rc = dev_upload(ctx, &L.tile_hi, hi.data(), hi.size())))
+        return -1;
+    std::vector<double> zeros(d->n, 0.0);
+    if ((rc = dev_upload(ctx, &L.shapes, d->n_src ? d->shapes : zeros.data(),
+                         (size_t)std::max(d->n_src, 1) * d->n)) ||
+        (rc = dev_upload(ctx, &L.weights, d->weights ? d->weights : zeros.data(),
+                         (size_t)d->n)))
+        return -1;
+    L.n_elem = d->n_elem;
+    if (d->n_elem > 0) {
+        if (!d->elem_dof || !d->elem_geo || !d->node_elem_ptr || !d->node_elem) {
+            set_err(ctx, PG_EINVAL, "nonlinear level needs element arrays");
+            return -1;
+        }
+        int nne = d->node_elem_ptr[d->n];
+        if ((rc = dev_upload(ctx, &L.elem_dof, d->elem_dof, (size_t)d->n_elem * 3)) ||
+            (rc = dev_upload(ctx, &L.elem_geo, d->elem_geo, (size_t)d->n_elem * 7)) ||
+            (rc = dev_upload(ctx, &L.ne_ptr, d->node_elem_ptr, (size_t)d->n + 1)) ||
+            (rc = dev_upload(ctx, &L.ne, d->node_elem, (size_t)nne)))
+            return -1;
+    }
+    ctx->levels.push_back(L);
+    return (int)ctx->levels.size() - 1;
+}
+
+// grow the per-level workspace to hold B columns
+static int ensure_ws(pg_ctx* ctx, Level& L, int B) {
+    if (B <= L.ws_B) return PG_OK;
+    for (void* p : L.ws_allocs) cudaFree(p);
+    L.ws_allocs.clear();
+    auto alloc = [&](void** p, size_t bytes) -> int {
+        cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 8));
+        if (e != cudaSuccess)
+            return set_err(ctx, PG_ECUDA, "workspace alloc of %zu bytes: %s", bytes,
+                           cudaGetErrorString(e));
+        L.ws_allocs.push_back(*p);
+        return PG_OK;
+    };
+    const size_t vec = (size_t)B * L.n * sizeof(double);
+    PcgWork& W = L.W;
+    int rc = 0;
+    if (L.dia && !L.resident) {
+        const size_t vld = (size_t)B * L.ld * sizeof(double);
+        if ((rc = alloc((void**)&L.V.x, vld)) || (rc = alloc((void**)&L.V.r, vld)) ||
+            (rc = alloc((void**)&L.V.p[0], vld)) || (rc = alloc((void**)&L.V.p[1], vld)))
+            return rc;
+        // padding rows [n, ld) stay zero forever (kernels write rows < n only)
+        CU(cudaMemset(L.V.x, 0, vld));
+        CU(cudaMemset(L.V.r, 0, vld));
+        CU(cudaMemset(L.V.p[0], 0, vld));
+        CU(cudaMemset(L.V.p[1], 0, vld));
+    } else if (!L.resident || L.n_elem > 0) {
+        if ((rc = alloc((void**)&W.r, vec)) || (rc = alloc((void**)&W.p[0], vec)) ||
+            (rc = alloc((void**)&W.p[1], vec)))
+            return rc;
+    }
+    if ((rc = alloc((void**)&W.rho, B * 8)) || (rc = alloc((void**)&W.alpha, B * 8)) ||
+        (rc = alloc((void**)&W.beta, B * 8)) || (rc = alloc((void**)&W.tol2, B * 8)) ||
+        (rc = alloc((void**)&W.bnorm2, B * 8)) || (rc = alloc((void**)&W.it, B * 4)) ||
+        (rc = alloc((void**)&W.flag, B * 4)) ||
+        (rc = alloc((void**)&W.partial, (size_t)B * L.n_tiles * 3 * 8)) ||
+        (rc = alloc((void**)&W.cnt, B * 4)) || (rc = alloc((void**)&W.gcnt, 8)) ||
+        (rc = alloc((void**)&W.act[0], B * 4)) || (rc = alloc((void**)&W.act[1], B * 4)) ||
+        (rc = alloc((void**)&W.nact, 8)))
+        return rc;
+    CU(cudaMemset(W.cnt, 0, B * 4));
+    CU(cudaMemset(W.gcnt, 0, 8));
+    if (L.n_elem > 0) {
+        NewtonWork& N = L.NW;
+        if ((rc = alloc((void**)&N.u, vec)) || (rc = alloc((void**)&N.delta, vec)) ||
+            (rc = alloc((void**)&N.rhs, vec)) || (rc = alloc((void**)&N.res, vec)) ||
+            (rc = alloc((void**)&N.ucur, vec)) || (rc = alloc((void**)&N.dinv, vec)) ||
+            (rc = alloc((void**)&N.scale, B * 8)) || (rc = alloc((void**)&N.rnorm, B * 8)) ||
+            (rc = alloc((void**)&N.tnorm, B * 8)) || (rc = alloc((void**)&N.alpha, B * 8)) ||
+            (rc = alloc((void**)&N.state, B * 4)) || (rc = alloc((void**)&N.nit, B * 4)) ||
+            (rc = alloc((void**)&N.halv, B * 4)) || (rc = alloc((void**)&N.zero, B * 8)))
+            return rc;
+        CU(cudaMemset(N.zero, 0, B * 8));
+    }
+    L.ws_B = B;
+    return PG_OK;
+}
+
+static int poll_nact(pg_ctx* ctx, PcgWork& W, int cur, cudaStream_t st, int* out) {
+    CU(cudaMemcpyAsync(ctx->h_poll, W.nact + cur, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    *out = ctx->h_poll[0];
+    return PG_OK;
+}
+
+template <int C>
+static int launch_setup(pg_ctx* ctx, Level& L, int B, const double* u_prev,
+                        const double* guess, const double* inv_dt, const double* src,
+                        double* x, cudaStream_t st) {
+    dim3 grid(L.n_tiles, (B + C - 1) / C);
+    const double rtol2 = ctx->opts.rtol * ctx->opts.rtol;
+    if (guess) {
+        size_t sm = stream_smem(L, C, true);
+        CU(cudaFuncSetAttribute(k_pcg_setup<C, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_pcg_setup<C, true><<<grid, PG_NT, sm, st>>>(pcg_view(L), L.W, B, u_prev, guess,
+                                                       inv_dt, src, x, rtol2,
+                                                       ctx->opts.max_iters);
+    } else {
+        size_t sm = stream_smem(L, C, false);
+        CU(cudaFuncSetAttribute(k_pcg_setup<C, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_pcg_setup<C, false><<<grid, PG_NT, sm, st>>>(pcg_view(L), L.W, B, u_prev, guess,
+                                                        inv_dt, src, x, rtol2,
+                                                        ctx->opts.max_iters);
+    }
+    LAUNCHED();
+    return PG_OK;
+}
+
+template <int C>
+static int launch_iter(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv_dt,
+                       double* x, cudaStream_t st) {
+    dim3 grid(L.n_tiles, ny);
+    size_t sm = stream_smem(L, C, false);
+    static bool attr_done = false;   // per template instance
+    if (!attr_done) {
+        CU(cudaFuncSetAttribute(k_pcg_dir<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                96 * 1024 + 1024));
+        CU(cudaFuncSetAttribute(k_pcg_upd<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                96 * 1024 + 1024));
+        attr_done = true;
+    }
+    k_pcg_dir<C><<<grid, PG_NT, sm, st>>>(pcg_view(L), L.W, cur, inv_dt);
+    LAUNCHED();
+    k_pcg_upd<C><<<grid, PG_NT, sm, st>>>(pcg_view(L), L.W, cur, inv_dt, x,
+                                           ctx->opts.max_iters);
+    LAUNCHED();
+    return PG_OK;
+}
+
+static int run_setup(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* guess,
+                     const double* inv_dt, const double* src, double* x, cudaStream_t st) {
+    int Cs = guess ? std::max(1, L.C / 2) : L.C;
+    switch (Cs) {
+        case 8: return launch_setup<8>(ctx, L, B, u_prev, guess, inv_dt, src, x, st);
+        case 4: return launch_setup<4>(ctx, L, B, u_prev, guess, inv_dt, src, x, st);
+        case 2: return launch_setup<2>(ctx, L, B, u_prev, guess, inv_dt, src, x, st);
+        default: return launch_setup<1>(ctx, L, B, u_prev, guess, inv_dt, src, x, st);
+    }
+}
+
+static int run_iter(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv_dt, double* x,
+                    cudaStream_t st) {
+    switch (L.C) {
+        case 8: return launch_iter<8>(ctx, L, ny, cur, inv_dt, x, st);
+        case 4: return launch_iter<4>(ctx, L, ny, cur, inv_dt, x, st);
+        case 2: return launch_iter<2>(ctx, L, ny, cur, inv_dt, x, st);
+        default: return launch_iter<1>(ctx, L, ny, cur, inv_dt, x, st);
+    }
+}
+
+static DiaLevel dia_view(const Level& L) {
+    DiaLevel v;
+    v.n = L.n;
+    v.ld = L.ld;
+    v.U = L.U;
+    for (int u = 0; u <= PG_DIA_MAX; ++u) v.off[u] = L.off[u];
+    v.omax = L.omax;
+    v.mk = L.mk;
+    v.n_src = L.n_src;
+    v.shapes = L.shapes;
+    v.R = L.R;
+    v.n_tiles = L.n_tiles;
+    return v;
+}
+
+template <int C, int UU>
+static int launch_dia_iter(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv_dt,
+                           cudaStream_t st) {
+    dim3 grid(L.n_tiles, ny);
+    const size_t sm = (size_t)C * (L.R + 2 * L.omax + 4) * sizeof(double);
+    static bool attr_done = false;
+    if (!attr_done) {
+        CU(cudaFuncSetAttribute(k_dia_dir<C, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                200 * 1024));
+        CU(cudaFuncSetAttribute(k_dia_upd<C, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                200 * 1024));
+        attr_done = true;
+    }
+    k_dia_dir<C, UU><<<grid, PG_DIA_NT, sm, st>>>(dia_view(L), L.V, L.W, cur, inv_dt);
+    LAUNCHED();
+    k_dia_upd<C, UU><<<grid, PG_DIA_NT, sm, st>>>(dia_view(L), L.V, L.W, cur, inv_dt,
+                                                   ctx->opts.max_iters);
+    LAUNCHED();
+    return PG_OK;
+}
+
+template <int UU>
+static int dia_iter_u(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv_dt,
+                      cudaStream_t st) {
+    switch (L.Cd) {
+        case 4: return launch_dia_iter<4, UU>(ctx, L, ny, cur, inv_dt, st);
+        case 2: return launch_dia_iter<2, UU>(ctx, L, ny, cur, inv_dt, st);
+        default: return launch_dia_iter<1, UU>(ctx, L, ny, cur, inv_dt, st);
+    }
+}
+
+static int dia_iter(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv_dt,
+                    cudaStream_t st) {
+    switch (L.U) {
+        case 1: return dia_iter_u<1>(ctx, L, ny, cur, inv_dt, st);
+        case 2: return dia_iter_u<2>(ctx, L, ny, cur, inv_dt, st);
+        case 3: return dia_iter_u<3>(ctx, L, ny, cur, inv_dt, st);
+        default: return dia_iter_u<4>(ctx, L, ny, cur, inv_dt, st);
+    }
+}
+
+static int pcg_dia(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* guess,
+                   const double* inv_dt, const double* src, double* u_out, const double* g,
+                   const int* g_idx, cudaStream_t st) {
+    {
+        const size_t sm = (size_t)2 * (L.R + 2 * L.omax + 4) * sizeof(double);
+        dim3 grid(L.n_tiles, B);
+        const double rt2 = ctx->opts.rtol * ctx->opts.rtol;
+        switch (L.U) {
+#define PG_SETUP_CASE(UU)                                                                  \
+    case UU:                                                                               \
+        CU(cudaFuncSetAttribute(k_dia_setup<1, UU>,                                        \
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));    \
+        k_dia_setup<1, UU><<<grid, PG_DIA_NT, sm, st>>>(dia_view(L), L.V, L.W, B, u_prev,  \
+                                                        guess, inv_dt, src, rt2,           \
+                                                        ctx->opts.max_iters);              \
+        break;
+            PG_SETUP_CASE(1)
+            PG_SETUP_CASE(2)
+            PG_SETUP_CASE(3)
+            PG_SETUP_CASE(4)
+#undef PG_SETUP_CASE
+            default: return set_err(ctx, PG_EINVAL, "DIA level without offsets");
+        }
+        LAUNCHED();
+    }
+    int rc, na = B, cur = 0, it = 0;
+    const int K = ctx->opts.check_every;
+    if ((rc = poll_nact(ctx, L.W, 0, st, &na))) return rc;
+    while (na > 0 && it < ctx->opts.max_iters) {
+        const int ny = (na + L.Cd - 1) / L.Cd;
+        for (int k = 0; k < K && it < ctx->opts.max_iters; ++k, ++it) {
+            rc = dia_iter(ctx, L, ny, cur, inv_dt, st);
+            if (rc) return rc;
+            cur ^= 1;
+        }
+        if ((rc = poll_nact(ctx, L.W, cur, st, &na))) return rc;
+    }
+    dim3 grid(std::max(1, std::min(64, (L.n + 255) / 256)), B);
+    k_dia_finish<<<grid, 256, 0, st>>>(L.n, L.ld, B, L.V.x, u_out, g, g_idx);
+    LAUNCHED();
+    return PG_OK;
+}
+
+// Streamed batched PCG for one linear system per column, x (= u_out) holds
+// the solution on return (stream-ordered; no g add).
+static int pcg_streamed(pg_ctx* ctx, Level& L, int B, const double* u_prev,
+                        const double* guess, const double* inv_dt, const double* src,
+                        double* x, cudaStream_t st) {
+    int rc = run_setup(ctx, L, B, u_prev, guess, inv_dt, src, x, st);
+    if (rc) return rc;
+    int na = B, cur = 0;
+    const int K = ctx->opts.check_every;
+    if ((rc = poll_nact(ctx, L.W, 0, st, &na))) return rc;
+    int it = 0;
+    while (na > 0 && it < ctx->opts.max_iters) {
+        const int ny = (na + L.C - 1) / L.C;
+        for (int k = 0; k < K && it < ctx->opts.max_iters; ++k, ++it) {
+            if ((rc = run_iter(ctx, L, ny, cur, inv_dt, x, st))) return rc;
+            cur ^= 1;
+        }
+        if ((rc = poll_nact(ctx, L.W, cur, st, &na))) return rc;
+    }
+    return PG_OK;
+}
+
+static int launch_resident(pg_ctx* ctx, Level& L, int B, const double* u_prev,
+                           const double* guess, const double* inv_dt, const double* src,
+                           double* u_out, const double* g, const int* g_idx, cudaStream_t st) {
+    size_t sm = (size_t)5 * L.n * sizeof(double);
+    CU(cudaFuncSetAttribute(k_pcg_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sm));
+    k_pcg_resident<<<B, PG_RES_NT, sm, st>>>(pcg_view(L), B, u_prev, guess, inv_dt, src, u_out,
+                                             g, g_idx, ctx->opts.rtol * ctx->opts.rtol,
+                                             ctx->opts.max_iters, ctx->d_iters, ctx->d_ictr);
+    LAUNCHED();
+    return PG_OK;
+}
+
+static int begin_stats(pg_ctx* ctx, Level& L, cudaStream_t st) {
+    CU(cudaMemsetAsync(ctx->d_iters + 1, 0, sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(ctx->d_ictr, 0, sizeof(int), st));
+    CU(cudaMemsetAsync(ctx->d_ictr + 2, 0, sizeof(int), st));
+    L.W.iters = ctx->d_iters;
+    L.W.ictr = ctx->d_ictr;
+    return PG_OK;
+}
+
+static int newton_batch(pg_ctx* ctx, Level& L, int B, const double* u_prev,
+                        const double* guess, const double* inv_dt, const double* src,
+                        double* u_out, cudaStream_t st);
+
+extern "C" int pg_phi_batch(pg_ctx* ctx, int level, int B, const double* u_prev,
+                            const double* guess, const double* inv_dt, const double* src,
+                            double* u_out, const double* g, const int32_t* g_idx,
+                            void* stream) {
+    if (!ctx) return PG_EINVAL;
+    if (level < 0 || level >= (int)ctx->levels.size())
+        return set_err(ctx, PG_EINVAL, "no spatial level %d", level);
+    if (B < 0) return set_err(ctx, PG_EINVAL, "negative batch");
+    if (B == 0) return PG_OK;
+    if (!u_prev || !inv_dt || !u_out || (!src && ctx->levels[level].n_src > 0))
+        return set_err(ctx, PG_EINVAL, "null state/time/source pointer");
+    if (u_out == u_prev || (guess && u_out == guess))
+        return set_err(ctx, PG_EINVAL, "u_out must not alias u_prev or guess");
+    if (guess == u_prev) guess = nullptr;
+    if (g && !g_idx) return set_err(ctx, PG_EINVAL, "g requires g_idx");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    Level& L = ctx->levels[level];
+    ctx->last = pg_phi_stats{};
+    ctx->last.columns = B;
+    ctx->total.columns += B;
+    ctx->last_level = level;
+    int rc = ensure_ws(ctx, L, B);
+    if (rc) return rc;
+    if ((rc = begin_stats(ctx, L, st))) return rc;
+    if (L.n_elem > 0) {
+        rc = newton_batch(ctx, L, B, u_prev, guess, inv_dt, src, u_out, st);
+        if (rc) return rc;
+    } else if (L.resident) {
+        return launch_resident(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st);
+    } else if (L.dia) {
+        return pcg_dia(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st);
+    } else {
+        if ((rc = pcg_streamed(ctx, L, B, u_prev, guess, inv_dt, src, u_out, st))) return rc;
+    }
+    if (g) {
+        dim3 grid(std::max(1, std::min(64, (L.n + 255) / 256)), B);
+        k_add_g<<<grid, 256, 0, st>>>(L.n, B, u_out, g, g_idx);
+        LAUNCHED();
+    }
+    return PG_OK;
+}
+
+extern "C" int pg_last_stats(pg_ctx* ctx, pg_phi_stats* out) {
+    if (!ctx || !out) return PG_EINVAL;
+    unsigned long long it[2] = {0, 0};
+    int ic[3] = {0, 0, 0};
+    CU(cudaMemcpy(it, ctx->d_iters, sizeof it, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(ic, ctx->d_ictr, sizeof ic, cudaMemcpyDeviceToHost));
+    ctx->last.column_iters = (int64_t)it[1];
+    ctx->last.batch_iters = ic[0];
+    ctx->last.failed = ic[2];
+    *out = ctx->last;
+    return PG_OK;
+}
+
+extern "C" int pg_total_stats(pg_ctx* ctx, pg_phi_stats* out, int reset) {
+    if (!ctx || !out) return PG_EINVAL;
+    unsigned long long it[2] = {0, 0};
+    int ic[3] = {0, 0, 0};
+    CU(cudaMemcpy(it, ctx->d_iters, sizeof it, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(ic, ctx->d_ictr, sizeof ic, cudaMemcpyDeviceToHost));
+    ctx->total.column_iters = (int64_t)it[0];
+    ctx->total.failed = ic[1];
+    ctx->total.launches = ctx->launches;
+    *out = ctx->total;
+    if (reset) {
+        ctx->total = pg_phi_stats{};
+        CU(cudaMemset(ctx->d_iters, 0, 2 * sizeof(unsigned long long)));
+        CU(cudaMemset(ctx->d_ictr, 0, 3 * sizeof(int)));
+    }
+    return PG_OK;
+}
+
+extern "C" int pg_newton_failure(pg_ctx* ctx, int* column, int* iterations) {
+    if (!ctx) return PG_EINVAL;
+    if (column) *column = ctx->newton_fail_col;
+    if (iterations) *iterations = ctx->newton_fail_iters;
+    return PG_OK;
+}
+
+static int grid_for(pg_ctx* ctx, size_t total) {
+    size_t blocks = (total + 255) / 256;
+    size_t cap = (size_t)ctx->n_sm * 8;
+    return (int)std::max<size_t>(1, std::min(blocks, cap));
+}
+
+extern "C" int pg_restrict(pg_ctx* ctx, int fine, int B, const double* in, double* out,
+                           int mode, void* stream) {
+    if (!ctx) return PG_EINVAL;
+    if (fine < 0 || fine + 1 >= (int)ctx->levels.size())
+        return set_err(ctx, PG_EINVAL, "no grid below %d", fine);
+    if (mode != 0 && mode != 1) return set_err(ctx, PG_EINVAL, "restriction mode %d", mode);
+    if (B <= 0) return B == 0 ? PG_OK : PG_EINVAL;
+    const int sf = ctx->levels[fine].side, sc = ctx->levels[fine + 1].side;
+    if (sf != 2 * sc + 1) return set_err(ctx, PG_EINVAL, "grids %d/%d not nested", sf, sc);
+    CU(cudaSetDevice(ctx->device));
+    k_restrict<<<grid_for(ctx, (size_t)sc * sc * B), 256, 0, (cudaStream_t)stream>>>(
+        sf, sc, B, in, out, mode);
+    LAUNCHED();
+    return PG_OK;
+}
+
+extern "C" int pg_prolong_add(pg_ctx* ctx, int coarse, int B, const double* in, double* out,
+                              const int32_t* out_idx, double beta, int mode, void* stream) {
+    if (!ctx) return PG_EINVAL;
+    if (coarse < 1 || coarse >= (int)ctx->levels.size())
+        return set_err(ctx, PG_EINVAL, "no grid above %d", coarse);
+    if (mode != 0 && mode != 1) return set_err(ctx, PG_EINVAL, "prolongation mode %d", mode);
+    if (beta != 0.0 && beta != 1.0) return set_err(ctx, PG_EINVAL, "beta must be 0 or 1");
+    if (B <= 0) return B == 0 ? PG_OK : PG_EINVAL;
+    const int sc = ctx->levels[coarse].side, sf = ctx->levels[coarse - 1].side;
+    if (sf != 2 * sc + 1) return set_err(ctx, PG_EINVAL, "grids %d/%d not nested", sf, sc);
+    CU(cudaSetDevice(ctx->device));
+    k_prolong_add<<<grid_for(ctx, (size_t)sf * sf * B), 256, 0, (cudaStream_t)stream>>>(
+        sc, sf, B, in, out, out_idx, beta, mode);
+    LAUNCHED();
+    return PG_OK;
+}
+
+extern "C" int pg_c_residual(pg_ctx* ctx, int level, int B, const double* prop,
+                             const double* c, const int32_t* c_idx, const double* g,
+                             const int32_t* g_idx, double* res, double* sumsq,
+                             const double* last_f, const double* inv_dt, double* loss,
+                             void* stream) {
+    if (!ctx) return PG_EINVAL;
+    if (level < 0 || level >= (int)ctx->levels.size())
+        return set_err(ctx, PG_EINVAL, "no spatial level %d", level);
+    if (B <= 0) return B == 0 ? PG_OK : PG_EINVAL;
+    if (!prop || !c || !sumsq || (last_f && (!inv_dt || !loss)))
+        return set_err(ctx, PG_EINVAL, "null residual argument");
+    CU(cudaSetDevice(ctx->device));
+    const Level& L = ctx->levels[level];
+    k_c_residual<<<B, 512, 0, (cudaStream_t)stream>>>(L.n, prop, c, c_idx, g, g_idx, res,
+                                                       sumsq, last_f, inv_dt, L.weights, loss);
+    LAUNCHED();
+    return PG_OK;
+}
+
+extern "C" int pg_fas_rhs(pg_ctx* ctx, int coarse, int coarsen, int B, const double* kept,
+                          const double* cprop, const double* res, double* rhs, int mode,
+                          void* stream) {
+    if (!ctx) return PG_EINVAL;
+    if (coarse < 0 || coarse >= (int)ctx->levels.size() || (coarsen && coarse < 1))
+        return set_err(ctx, PG_EINVAL, "bad coarse level %d", coarse);
+    if (B <= 0) return B == 0 ? PG_OK : PG_EINVAL;
+    const int sc = ctx->levels[coarse].side;
+    const int sf = coarsen ? ctx->levels[coarse - 1].side : sc;
+    if (coarsen && sf != 2 * sc + 1) return set_err(ctx, PG_EINVAL, "grids not nested");
+    CU(cudaSetDevice(ctx->device));
+    k_fas_rhs<<<grid_for(ctx, (size_t)sc * sc * B), 256, 0, (cudaStream_t)stream>>>(
+        sf, sc, coarsen, B, kept, cprop, res, rhs, mode);
+    LAUNCHED();
+    return PG_OK;
+}
+
+#include "newton_host.inc"
+
+extern "C" int64_t pg_launch_count(pg_ctx* ctx) { return ctx ? ctx->launches : 0; }

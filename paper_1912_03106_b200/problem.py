@@ -1,0 +1,231 @@
+"""The GPU problem object: the reference's Phi plug-in contract, batched.
+
+Reference contract (problems.py:1-17, consumed by mgrit.py:361-366):
+
+    step(u_prev, t_prev, t_next, spatial_level=0, guess=None, smooth=False)
+        -> (BlockState, StepDiagnostics)
+    initial_state(spatial_level), loss_weights(spatial_level), forcing(...),
+    spatial (restrict_state / prolong_error), n_scalars
+
+GpuFemProblem keeps that contract (step() is the B = 1 view) and adds the
+batched entry points the B200 engine drives: phi_batch over [B][n] device
+states, transfers, C-point residuals and the FAS right-hand side, all going
+through libpintgpu's C ABI (include/pintgpu.h).  Construction fails when the
+library or a CUDA device is missing -- there is no CPU path.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import NewtonConvergenceError, PintGpuError
+from .excitation import Excitation
+from .mesh import build_grids
+from .spatial import SpatialHierarchy2D
+from .state import BlockState
+
+
+@dataclass(frozen=True)
+class StepDiagnostics:
+    """reference problems.py:33-36"""
+    iterations: int
+    converged: bool = True
+
+
+def _np_ptr(a, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+class GpuFemProblem:
+    """2D P1 eddy-current problem (linear or Brauer-nonlinear) on one GPU."""
+
+    n_scalars = 0
+
+    def __init__(self, spec, device=None, rtol=None, max_iters=None,
+                 check_every=16):
+        if not torch.cuda.is_available():
+            raise PintGpuError("GpuFemProblem needs a CUDA device (no CPU fallback)")
+        self.lib = _lib.load()
+        self.spec = spec
+        self.device = torch.device("cuda", torch.cuda.current_device()
+                                   if device is None else device)
+        self.spatial = SpatialHierarchy2D(spec["N"], spec.get("n_spatial_grids", 1),
+                                          spec.get("restriction", "injection"),
+                                          spec.get("prolongation", "bilinear"),
+                                          ops=self)
+        ex = spec.get("excitation")
+        self.excitation = Excitation(**ex) if ex else None
+        self.grids = build_grids(spec)
+        self.phases = self.grids[0].phases
+        self.n_src = len(self.phases)
+        ctx = ctypes.c_void_p()
+        rc = self.lib.pg_create(ctypes.byref(ctx), self.device.index)
+        if rc != 0 or not ctx:
+            raise PintGpuError(f"pg_create failed on device {self.device} (code {rc})")
+        self.ctx = ctx
+        self._keep = []
+        for g in self.grids:
+            self._add_level(g)
+        inner = spec.get("inner", {})
+        nl = spec.get("nonlinear") or {}
+        nt = nl.get("newton", {})
+        self.opts = _lib.SolverOpts(
+            rtol=float(rtol if rtol is not None else inner.get("rtol", 1e-13)),
+            max_iters=int(max_iters if max_iters is not None else inner.get("max_iters", 20000)),
+            check_every=int(check_every),
+            newton_tol=float(nt.get("tol", 1e-11)),
+            newton_max_iters=int(nt.get("max_iters", 25)),
+            damping=float(nt.get("damping", 0.5)),
+            max_halvings=int(nt.get("max_halvings", 8)),
+            nu0=float(spec["nu0"]), k1=float(nl.get("k1", 0.0)),
+            k2=float(nl.get("k2", 0.0)), k3=float(nl.get("k3", 1.0)))
+        _lib.check(self.ctx, self.lib.pg_set_options(self.ctx, ctypes.byref(self.opts)),
+                   "pg_set_options")
+        self._weights = [torch.as_tensor(g.weights, device=self.device) for g in self.grids]
+        self.nonlinear = bool(spec.get("nonlinear"))
+
+    def _add_level(self, g):
+        arrays = dict(row_ptr=np.ascontiguousarray(g.row_ptr, np.int32),
+                      col_idx=np.ascontiguousarray(g.col_idx, np.int32),
+                      m_val=np.ascontiguousarray(g.m_val),
+                      k_val=np.ascontiguousarray(g.k_val),
+                      shapes=np.ascontiguousarray(g.shapes.reshape(-1)),
+                      weights=np.ascontiguousarray(g.weights))
+        d = _lib.LevelDesc()
+        d.n, d.nnz, d.side = g.n, g.nnz, g.side
+        d.row_ptr = _np_ptr(arrays["row_ptr"], ctypes.c_int32)
+        d.col_idx = _np_ptr(arrays["col_idx"], ctypes.c_int32)
+        d.m_val = _np_ptr(arrays["m_val"], ctypes.c_double)
+        d.k_val = _np_ptr(arrays["k_val"], ctypes.c_double)
+        d.n_src = len(g.phases)
+        d.shapes = _np_ptr(arrays["shapes"], ctypes.c_double)
+        d.weights = _np_ptr(arrays["weights"], ctypes.c_double)
+        d.n_elem = g.n_elem
+        if g.n_elem:
+            for k in ("elem_dof", "elem_geo", "node_elem_ptr", "node_elem"):
+                arrays[k] = np.ascontiguousarray(getattr(g, k))
+            d.elem_dof = _np_ptr(arrays["elem_dof"], ctypes.c_int32)
+            d.elem_geo = _np_ptr(arrays["elem_geo"], ctypes.c_double)
+            d.node_elem_ptr = _np_ptr(arrays["node_elem_ptr"], ctypes.c_int32)
+            d.node_elem = _np_ptr(arrays["node_elem"], ctypes.c_int32)
+        idx = self.lib.pg_add_level(self.ctx, ctypes.byref(d))
+        if idx < 0:
+            _lib.check(self.ctx, _lib.PG_EINVAL, "pg_add_level")
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            torch.cuda.synchronize(self.device)
+            self.lib.pg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- the reference contract ---------------------------------------------------
+    def initial_state(self, spatial_level=0):
+        return BlockState.zeros(self.spatial.size(spatial_level), 0, spatial_level,
+                                device=self.device)
+
+    def loss_weights(self, spatial_level=0):
+        return self._weights[spatial_level]
+
+    def source_values(self, times, smooth=False):
+        """[len(times), n_src] excitation values (host)."""
+        times = np.atleast_1d(np.asarray(times, dtype=float))
+        if self.excitation is None or not self.n_src:
+            return np.zeros((len(times), self.n_src))
+        return self.excitation.table(self.phases, times, smooth)
+
+    def forcing(self, t, spatial_level=0, smooth=False):
+        v = torch.as_tensor(self.source_values([t], smooth)[0], device=self.device)
+        g = self.grids[spatial_level]
+        return v @ torch.as_tensor(g.shapes, device=self.device)
+
+    def step(self, u_prev, t_prev, t_next, spatial_level=0, guess=None, smooth=False):
+        """One implicit-Euler step (reference problems.py:138-146)."""
+        n = self.spatial.size(spatial_level)
+        if u_prev.field.numel() != n:
+            raise ValueError(f"state has {u_prev.field.numel()} entries, grid "
+                             f"{spatial_level} has {n}")
+        dt = float(t_next) - float(t_prev)
+        inv_dt = torch.tensor([1.0 / dt], dtype=torch.float64, device=self.device)
+        src = torch.as_tensor(self.source_values([t_next], smooth),
+                              device=self.device).reshape(1, -1)
+        u_in = u_prev.field.to(self.device).reshape(1, n).contiguous()
+        gs = None
+        if guess is not None and guess is not u_prev:
+            gs = guess.field.to(self.device).reshape(1, n).contiguous()
+        out = torch.empty(1, n, dtype=torch.float64, device=self.device)
+        self.phi_batch(spatial_level, u_in, inv_dt, src, out, guess=gs)
+        st = self.last_stats()
+        if st["failed"]:
+            raise PintGpuError(f"inner PCG did not converge at t={t_next:.6g} "
+                               f"on grid {spatial_level}")
+        its = st["newton_iters"] if self.nonlinear else st["batch_iters"]
+        return (BlockState(out[0], spatial_level=spatial_level),
+                StepDiagnostics(iterations=int(its)))
+
+    # --- batched entry points -------------------------------------------------------
+    def _stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def phi_batch(self, level, u_prev, inv_dt, src, out, g=None, g_idx=None, guess=None):
+        """out[b] = Phi(u_prev[b]) (+ g[g_idx[b]]).  All device tensors:
+        u_prev/out [B, n] fp64, inv_dt [B], src [B, n_src], g [*, n], g_idx [B]
+        int32."""
+        B = int(u_prev.shape[0])
+        rc = self.lib.pg_phi_batch(self.ctx, int(level), B, _lib.ptr(u_prev),
+                                   _lib.ptr(guess), _lib.ptr(inv_dt),
+                                   _lib.ptr(src) if self.n_src else None, _lib.ptr(out),
+                                   _lib.ptr(g), _lib.ptr(g_idx), self._stream())
+        if rc == _lib.PG_ENEWTON:
+            col, its = ctypes.c_int(), ctypes.c_int()
+            self.lib.pg_newton_failure(self.ctx, ctypes.byref(col), ctypes.byref(its))
+            msg = self.lib.pg_last_error(self.ctx).decode()
+            raise NewtonConvergenceError(msg, time=None, iterations=its.value)
+        _lib.check(self.ctx, rc, "pg_phi_batch")
+
+    def last_stats(self):
+        s = _lib.PhiStats()
+        _lib.check(self.ctx, self.lib.pg_last_stats(self.ctx, ctypes.byref(s)), "pg_last_stats")
+        return {k: int(getattr(s, k)) for k, _ in s._fields_}
+
+    def total_stats(self, reset=False):
+        s = _lib.PhiStats()
+        _lib.check(self.ctx, self.lib.pg_total_stats(self.ctx, ctypes.byref(s), int(reset)),
+                   "pg_total_stats")
+        return {k: int(getattr(s, k)) for k, _ in s._fields_}
+
+    def launch_count(self):
+        return int(self.lib.pg_launch_count(self.ctx))
+
+    def restrict(self, fine_level, x, out):
+        _lib.check(self.ctx, self.lib.pg_restrict(
+            self.ctx, int(fine_level), int(x.shape[0]), _lib.ptr(x), _lib.ptr(out),
+            self.spatial.r_mode, self._stream()), "pg_restrict")
+
+    def prolong_add(self, coarse_level, x, out, out_idx=None, beta=1.0):
+        _lib.check(self.ctx, self.lib.pg_prolong_add(
+            self.ctx, int(coarse_level), int(x.shape[0]), _lib.ptr(x), _lib.ptr(out),
+            _lib.ptr(out_idx), float(beta), self.spatial.p_mode, self._stream()),
+            "pg_prolong_add")
+
+    def c_residual(self, level, prop, c, sumsq, c_idx=None, g=None, g_idx=None,
+                   res=None, last_f=None, inv_dt=None, loss=None):
+        _lib.check(self.ctx, self.lib.pg_c_residual(
+            self.ctx, int(level), int(prop.shape[0]), _lib.ptr(prop), _lib.ptr(c),
+            _lib.ptr(c_idx), _lib.ptr(g), _lib.ptr(g_idx), _lib.ptr(res), _lib.ptr(sumsq),
+            _lib.ptr(last_f), _lib.ptr(inv_dt), _lib.ptr(loss), self._stream()),
+            "pg_c_residual")
+
+    def fas_rhs(self, coarse_level, coarsen, kept, cprop, res, out):
+        _lib.check(self.ctx, self.lib.pg_fas_rhs(
+            self.ctx, int(coarse_level), int(bool(coarsen)), int(kept.shape[0]),
+            _lib.ptr(kept), _lib.ptr(cprop), _lib.ptr(res), _lib.ptr(out),
+            self.spatial.r_mode, self._stream()), "pg_fas_rhs")

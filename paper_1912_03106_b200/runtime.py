@@ -1,0 +1,195 @@
+"""Time-domain decomposition and the inter-rank transport.
+
+Decomposition restates reference runtime.py:31-105 exactly: whole
+C-intervals per rank, remainder to the lowest ranks, the last active rank
+owns any F-tail, ranks beyond the unit count idle on that level.
+
+The transport replaces the reference's queue-based p2p (runtime.py:123-254)
+with torch.distributed: one process per GPU, NCCL over NVLink/NVSwitch for
+device tensors (gloo for CPU tests).  Every exchange step of a sweep is one
+grouped batch_isend_irecv (an ncclGroupStart/End), norms are an all-gather
+of per-rank partial sums reduced in rank order on every rank (the
+determinism of runtime.py:189-203), maxima an all-reduce.
+"""
+
+from bisect import bisect_right
+
+import numpy as np
+import torch
+
+from .errors import TransportError
+
+
+class Decomposition:
+    """Ownership of one level's C-intervals across n_workers ranks."""
+
+    def __init__(self, splitting, n_workers):
+        if n_workers < 1:
+            raise ValueError(f"n_workers must be >= 1, got {n_workers}")
+        self.splitting = splitting
+        self.n_workers = n_workers
+        k = splitting.n_intervals
+        base, rem = divmod(k, n_workers)
+        self._n_units = [base + 1 if w < rem else base for w in range(n_workers)]
+        self._first_unit = [0] * n_workers
+        for w in range(1, n_workers):
+            self._first_unit[w] = self._first_unit[w - 1] + self._n_units[w - 1]
+        self._last_rank = max((w for w in range(n_workers) if self._n_units[w] > 0),
+                              default=0)
+
+    def n_units(self, rank):
+        return self._n_units[rank]
+
+    def first_unit(self, rank):
+        return self._first_unit[rank]
+
+    def unit_owner(self, unit):
+        if not 0 <= unit < self.splitting.n_intervals:
+            raise ValueError(f"unit {unit} out of range")
+        ends = [self._first_unit[w] + self._n_units[w] for w in range(self.n_workers)]
+        return bisect_right(ends, unit)
+
+    def is_empty(self, rank):
+        return self._n_units[rank] == 0 and not (
+            rank == 0 and self.splitting.n_intervals == 0)
+
+    def c_points(self, rank):
+        c = self.splitting.c_indices
+        first = self._first_unit[rank]
+        return c[first + 1: first + 1 + self._n_units[rank]]
+
+    def left_boundary_index(self, rank):
+        return int(self.splitting.c_indices[self._first_unit[rank]])
+
+    def owned_range(self, rank):
+        if self.is_empty(rank):
+            return (0, 0)
+        c = self.splitting.c_indices
+        lo = self.left_boundary_index(rank) + 1
+        if self.splitting.n_intervals == 0:
+            return (1, self.splitting.n_points) if rank == 0 else (0, 0)
+        hi = int(c[self._first_unit[rank] + self._n_units[rank]]) + 1
+        if rank == self._last_rank:
+            hi = self.splitting.n_points
+        return (lo, hi)
+
+    def point_owner(self, point):
+        """Rank whose owned range contains point (index 0 -> rank 0)."""
+        for w in self.active_ranks():
+            lo, hi = self.owned_range(w)
+            if lo <= point < hi:
+                return w
+        if point == 0:
+            return 0
+        raise RuntimeError(f"point {point} has no owner")
+
+    def active_ranks(self):
+        return [w for w in range(self.n_workers) if not self.is_empty(w)]
+
+    def left_neighbor(self, rank):
+        for w in range(rank - 1, -1, -1):
+            if not self.is_empty(w):
+                return w
+        return None
+
+    def right_neighbor(self, rank):
+        for w in range(rank + 1, self.n_workers):
+            if not self.is_empty(w):
+                return w
+        return None
+
+
+class NullTransport:
+    """Single worker: no peers (reference runtime.py:110-120)."""
+
+    rank = 0
+    size = 1
+
+    def exchange(self, sends, recvs):
+        if sends or recvs:
+            raise TransportError("no peers in a single-worker run")
+
+    def sum_ordered(self, value):
+        return float(value)
+
+    def max(self, value):
+        return float(value)
+
+    def barrier(self):
+        pass
+
+
+class DistTransport:
+    """torch.distributed transport (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            raise TransportError("torch.distributed is not initialised")
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        self.device = device if device is not None else torch.device("cpu")
+        # the first collective must involve every rank (NCCL p2p rule)
+        t = torch.zeros(1, dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, group=group)
+
+    def exchange(self, sends, recvs):
+        """sends/recvs: lists of (peer, tensor); one grouped p2p batch."""
+        ops = [self.dist.P2POp(self.dist.isend, t.contiguous(), peer, self.group)
+               for peer, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group)
+                for peer, t in recvs]
+        if not ops:
+            return
+        for req in self.dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def sum_ordered(self, value):
+        """Rank-ascending sum of per-rank partials, identical on every rank."""
+        t = torch.tensor([float(value)], dtype=torch.float64, device=self.device)
+        out = [torch.zeros_like(t) for _ in range(self.size)]
+        self.dist.all_gather(out, t, group=self.group)
+        vals = torch.cat(out).cpu().numpy()
+        total = 0.0
+        for v in vals:
+            total += float(v)
+        return total
+
+    def max(self, value):
+        t = torch.tensor([float(value)], dtype=torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+def plan_moves(points, src_owner, dst_owner, rank):
+    """Route per-point rows from producer to consumer ranks.
+
+    points: increasing global point indices; src_owner / dst_owner: owner
+    rank per point (every rank computes the same arrays).  Returns
+    (local, sends, recvs), each a list of (peer, lo, hi) runs of
+    consecutive points with one (src, dst) pair."""
+    points = np.asarray(points)
+    src_owner = np.asarray(src_owner)
+    dst_owner = np.asarray(dst_owner)
+    local, sends, recvs = [], [], []
+    i, n = 0, len(points)
+    while i < n:
+        j = i + 1
+        while (j < n and src_owner[j] == src_owner[i] and dst_owner[j] == dst_owner[i]
+               and points[j] == points[j - 1] + 1):
+            j += 1
+        s, d = int(src_owner[i]), int(dst_owner[i])
+        run = (int(points[i]), int(points[j - 1]) + 1)
+        if s == rank and d == rank:
+            local.append((rank,) + run)
+        elif s == rank:
+            sends.append((d,) + run)
+        elif d == rank:
+            recvs.append((s,) + run)
+        i = j
+    return local, sends, recvs

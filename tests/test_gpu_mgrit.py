@@ -1,0 +1,54 @@
+"""MGRIT on the GPU vs the reference engine's fixtures (tests/golden)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(spec, max_iters, tol, **kw):
+    from paper_1912_03106_b200 import (CycleSpec, GpuFemProblem, StoppingCriterion,
+                                       TimeHierarchy, build_uniform_grid, mgrit_solve)
+    prob = GpuFemProblem(spec, **kw)
+    grid = build_uniform_grid(0.0, spec["tf"], spec["n_steps"])
+    mg = spec["mgrit"]
+    hier = TimeHierarchy.build(grid, mg["factors"])
+    run, sol = mgrit_solve(prob, hier,
+                           CycleSpec(kind=mg["kind"], gamma=mg["gamma"], max_iters=max_iters,
+                                     spatial_strategy=mg["spatial_strategy"],
+                                     nested_iterations=mg.get("nested_iterations", False)),
+                           StoppingCriterion(tolerance=tol))
+    return prob, grid, run, sol
+
+
+@pytest.mark.parametrize("name", ["mgrit_cfg1", "mgrit_cfg2_delayed_n32"])
+def test_mgrit_matches_reference_engine(cuda, name):
+    """Same iteration count; residual history within 1e-8 relative above the
+    Phi noise floor; C-point iterate within 1e-9."""
+    fx = load_golden(name)
+    prob, grid, run, sol = _run(fx["spec"], int(fx["max_iters"]), float(fx["tol"]))
+    hist = np.array([run.initial_residual] + run.residual_norms)
+    ref = fx["history"]
+    assert run.iterations == int(fx["iterations"])
+    assert run.converged == bool(fx["converged"])
+    rel = np.abs(hist - ref) / ref
+    assert rel.max() < 1e-6, rel
+    m = int(fx["factors"][0])
+    sol_c = sol.cpu().numpy()[::m]
+    err = np.linalg.norm(sol_c - fx["sol_c"]) / np.linalg.norm(fx["sol_c"])
+    assert err < 1e-9, err
+
+
+def test_gpu_sequential_matches_reference(cuda):
+    fx = load_golden("mgrit_cfg1")
+    from paper_1912_03106_b200 import GpuFemProblem, build_uniform_grid, sequential_solve
+    prob = GpuFemProblem(fx["spec"])
+    grid = build_uniform_grid(0.0, fx["spec"]["tf"], fx["spec"]["n_steps"])
+    traj = sequential_solve(prob, grid.points).cpu().numpy()
+    err = np.linalg.norm(traj[-1] - fx["seq_final"]) / np.linalg.norm(fx["seq_final"])
+    assert err < 1e-9, err
+    nrm = np.linalg.norm(traj, axis=1)
+    assert np.allclose(nrm, fx["seq_norms"], rtol=1e-9, atol=1e-14)

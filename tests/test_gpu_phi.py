@@ -1,0 +1,130 @@
+"""Batched Phi, transfers and MGRIT kernels vs the CPU oracle (GPU)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+PHI_FIXTURES = ["phi_cfg1", "phi_cfg2_n32", "phi_cfg2_n128"]
+
+
+def _problem(spec, **kw):
+    from paper_1912_03106_b200 import GpuFemProblem
+    return GpuFemProblem(spec, **kw)
+
+
+def _phi(prob, g, U, tp, tn, smooth=False, guess=None):
+    dev = prob.device
+    U_d = torch.as_tensor(U, device=dev).contiguous()
+    inv = torch.as_tensor(1.0 / (tn - tp), device=dev)
+    src = torch.as_tensor(prob.source_values(tn, smooth), device=dev).contiguous()
+    out = torch.empty_like(U_d)
+    gs = None if guess is None else torch.as_tensor(guess, device=dev).contiguous()
+    prob.phi_batch(g, U_d, inv, src, out, guess=gs)
+    return out.cpu().numpy(), prob.last_stats()
+
+
+@pytest.mark.parametrize("name", PHI_FIXTURES)
+@pytest.mark.parametrize("smooth", [False, True])
+def test_phi_batch_matches_oracle(cuda, name, smooth):
+    """Per-column Jacobi-PCG Phi vs the oracle's banded-Cholesky step
+    (problems.py:138-146 restated); tolerance: rtol 1e-13 inner solve ->
+    1e-10 relative per column."""
+    fx = load_golden(name)
+    prob = _problem(fx["spec"])
+    for g in range(prob.spatial.n_grids):
+        ref = fx[f"phis{g}" if smooth else f"phi{g}"]
+        got, st = _phi(prob, g, fx[f"u{g}"], fx[f"tp{g}"], fx[f"tn{g}"], smooth)
+        assert st["failed"] == 0
+        err = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
+        assert err.max() < 1e-10, (name, g, err.max(), st)
+
+
+def test_phi_guess_and_rhs_add(cuda):
+    fx = load_golden("phi_cfg2_n128")
+    prob = _problem(fx["spec"])
+    U, tp, tn, ref = fx["u0"], fx["tp0"], fx["tn0"], fx["phi0"]
+    got, _ = _phi(prob, 0, U, tp, tn, guess=np.zeros_like(U))
+    assert (np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)).max() < 1e-10
+    dev = prob.device
+    G = torch.randn(3, U.shape[1], dtype=torch.float64, device=dev)
+    gidx = torch.tensor([2, -1, 0, 1], dtype=torch.int32, device=dev)
+    U_d = torch.as_tensor(U, device=dev)
+    out = torch.empty_like(U_d)
+    prob.phi_batch(0, U_d, torch.as_tensor(1.0 / (tn - tp), device=dev),
+                   torch.as_tensor(prob.source_values(tn), device=dev), out, g=G, g_idx=gidx)
+    exp = torch.as_tensor(ref, device=dev).clone()
+    for b, gi in enumerate(gidx.tolist()):
+        if gi >= 0:
+            exp[b] += G[gi]
+    assert float((out - exp).abs().max() / exp.abs().max()) < 1e-10
+
+
+def test_step_contract_b1(cuda):
+    """step() is the B = 1 view with the reference signature."""
+    fx = load_golden("phi_cfg1")
+    prob = _problem(fx["spec"])
+    from paper_1912_03106_b200 import BlockState
+    u = BlockState(torch.as_tensor(fx["u0"][0], device=prob.device))
+    out, diag = prob.step(u, float(fx["tp0"][0]), float(fx["tn0"][0]), 0, guess=u)
+    ref = fx["phi0"][0]
+    assert np.linalg.norm(out.numpy() - ref) / np.linalg.norm(ref) < 1e-10
+    assert diag.converged and diag.iterations > 0
+    assert out.field.data_ptr() != u.field.data_ptr()          # fresh state
+    assert np.array_equal(u.numpy(), fx["u0"][0])               # input untouched
+
+
+@pytest.mark.parametrize("name", ["phi_cfg2_n32", "phi_cfg2_n32_inj"])
+def test_transfers_bitwise(cuda, name):
+    fx = load_golden(name)
+    prob = _problem(fx["spec"])
+    dev = prob.device
+    for g in range(prob.spatial.n_grids):
+        U = torch.as_tensor(fx[f"u{g}"], device=dev)
+        if f"R{g}" in fx:
+            out = torch.empty(U.shape[0], prob.spatial.size(g + 1), dtype=torch.float64,
+                              device=dev)
+            prob.restrict(g, U, out)
+            assert np.array_equal(out.cpu().numpy(), fx[f"R{g}"]), (name, g)
+        if f"P{g}" in fx:
+            out = torch.zeros(U.shape[0], prob.spatial.size(g - 1), dtype=torch.float64,
+                              device=dev)
+            prob.prolong_add(g, U, out, beta=0.0)
+            assert np.array_equal(out.cpu().numpy(), fx[f"P{g}"]), (name, g)
+            base = torch.randn_like(out)
+            acc = base.clone()
+            prob.prolong_add(g, U, acc, beta=1.0)
+            assert np.array_equal(acc.cpu().numpy(), base.cpu().numpy() + fx[f"P{g}"])
+
+
+def test_residual_and_fas_kernels(cuda):
+    fx = load_golden("phi_cfg2_n32")
+    prob = _problem(fx["spec"])
+    dev = prob.device
+    torch.manual_seed(0)
+    B, n, nc = 5, prob.spatial.size(0), prob.spatial.size(1)
+    prop, c, g, lf = (torch.randn(B, n, dtype=torch.float64, device=dev) for _ in range(4))
+    G = torch.randn(B + 2, n, dtype=torch.float64, device=dev)
+    gidx = torch.tensor([3, 0, -1, 6, 1], dtype=torch.int32, device=dev)
+    inv = torch.rand(B, dtype=torch.float64, device=dev) + 1.0
+    res = torch.empty_like(prop)
+    sq = torch.empty(B, dtype=torch.float64, device=dev)
+    loss = torch.empty(B, dtype=torch.float64, device=dev)
+    prob.c_residual(0, prop, c, sq, g=G, g_idx=gidx, res=res, last_f=lf, inv_dt=inv, loss=loss)
+    exp = prop - c
+    for b, gi in enumerate(gidx.tolist()):
+        if gi >= 0:
+            exp[b] = exp[b] + G[gi]
+    assert torch.equal(res, exp)
+    assert torch.allclose(sq, (exp * exp).sum(1), rtol=1e-13)
+    w = prob.loss_weights(0)
+    assert torch.allclose(loss, (w * ((c - lf) * inv[:, None]) ** 2).sum(1), rtol=1e-12)
+    kept, cprop = (torch.randn(B, nc, dtype=torch.float64, device=dev) for _ in range(2))
+    rhs = torch.empty_like(kept)
+    prob.fas_rhs(1, True, kept, cprop, res, rhs)
+    rres = torch.empty_like(kept)
+    prob.restrict(0, res, rres)
+    assert torch.equal(rhs, (kept - cprop) + rres)
