@@ -25,9 +25,11 @@
 #pragma once
 #include "common.cuh"
 #include "pcg.cuh"
+#include "tma.cuh"
 
 #define PG_DIA_MAX 4          // max upper offsets (7-point stencil uses 3)
 #define PG_DIA_NT 256
+#define PG_PT_NT 512          // threads of the persistent tile kernels
 
 struct DiaLevel {
     int n, ld;
@@ -194,13 +196,95 @@ k_dia_setup(DiaLevel L, DiaWork V, PcgWork W, int B, const double* __restrict__ 
     }
 }
 
-// --- direction update + SpMV + p.q --------------------------------------------------
+
+// CTA partial sum of NV values (no trailing barrier: callers pass another
+// __syncthreads before `red` is rewritten).  Result valid in thread 0.
+template <int NV, int NT>
+__device__ __forceinline__ void cta_partial_nt(double (&v)[NV], double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) red[warp * NV + k] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = 0.0;
+            for (int w = 0; w < NT / 32; ++w) s += red[w * NV + k];
+            v[k] = s;
+        }
+    }
+}
+
+__device__ __forceinline__ double ld_cg(const double* p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+// Warp-0 deferred finalize: after one fence per CTA, count this CTA's tiles
+// in and, for columns whose last tile this was, sum the per-tile partials
+// (fixed lane-strided order + shuffle tree: deterministic).
+template <typename F>
+__device__ __forceinline__ void finalize_columns(const PcgWork& W, int n_tiles, int cur,
+                                                 int j0, int na, int kper, int comp, F&& fin) {
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence();
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    for (int s = j0; s < na; s += kper) {
+        const int b = W.act[cur][s];
+        unsigned prev = 0;
+        if (lane == 0) prev = atomicAdd(&W.cnt[b], 1u);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev != (unsigned)(n_tiles - 1)) continue;
+        if (lane == 0) W.cnt[b] = 0u;
+        __threadfence();
+        double a = 0.0, c = 0.0;
+        const double* pp = W.partial + (size_t)b * n_tiles * 3;
+        for (int t = lane; t < n_tiles; t += 32) {
+            a += ld_cg(pp + 3 * t + comp);
+            if (comp == 1) c += ld_cg(pp + 3 * t + 2);
+        }
+        a = warp_sum(a);
+        c = warp_sum(c);
+        if (lane == 0) fin(b, a, c);
+    }
+}
+
+// --- persistent, TMA-pipelined iteration kernels ---------------------------------
+// Grid = n_tiles * k CTAs; CTA (tile = blockIdx.x % n_tiles, j = blockIdx.x /
+// n_tiles) walks the active columns j, j+k, j+2k, ...  Each work item's halo
+// (and own rows) arrive by cp.async.bulk into a 2-stage smem ring, so the
+// next column streams in while the current one is computed; the tile's
+// matrix rows stay hot in L1 across the columns a CTA visits.
+
+// --- v4: SpMV/direction kernel + streaming update kernel -------------------------
+//
+//   k_sdir (tile, C columns): TMA-stage the r and p_old halos of C columns
+//          (one mbarrier), p_new = D^-1 r + beta p_old in place, q = A p_new
+//          with each matrix row loaded once into registers and applied to all
+//          C columns; writes p_new and q (own rows), partial p.q.   32 n B
+//   k_supd (chunk, column): x += alpha p, r -= alpha q, partial r.z, r.r -
+//          a pure stream (no halo, no smem).                           48 n B
+//
+// 80 n bytes per column-iteration (16 n more than the 2-SpMV variant) but
+// each kernel is shaped for the memory system: one halo-staged SpMV, one
+// perfectly coalesced stream.  Cross-CTA reductions are deferred: partials
+// per (column, tile|chunk), one fence per CTA, warp-parallel finalize by the
+// CTA that completes a column.
+
 template <int C, int UU>
-__global__ void __launch_bounds__(PG_DIA_NT, 2)
-k_dia_dir(DiaLevel L, DiaWork V, PcgWork W, int cur, const double* __restrict__ inv_dt) {
-    extern __shared__ double smem[];
-    __shared__ double red[(PG_DIA_NT / 32)];
-    __shared__ int s_flag;
+__global__ void __launch_bounds__(PG_DIA_NT, 3)
+k_sdir(DiaLevel L, DiaWork V, PcgWork W, double* __restrict__ qv, int cur,
+       const double* __restrict__ inv_dt, int SPAN) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ double red[(PG_DIA_NT / 32) * C];
     const int na = W.nact[cur];
     const int slot0 = blockIdx.y * C;
     if (slot0 >= na) return;
@@ -208,185 +292,204 @@ k_dia_dir(DiaLevel L, DiaWork V, PcgWork W, int cur, const double* __restrict__ 
     int r0, r1, lo, hi;
     tile_span(L, tile, r0, r1, lo, hi);
     const int span = hi - lo;
+    const int nc = min(C, na - slot0);
     const double* __restrict__ p_old = V.p[cur];
     double* __restrict__ p_new = V.p[cur ^ 1];
-    const int nc = min(C, na - slot0);
-
-    // stage p_new = D^-1 r + beta p_old over the halo window, column by column
-    for (int c = 0; c < nc; ++c) {
-        const int b = W.act[cur][slot0 + c];
-        const double cb = inv_dt[b];
-        const double beta = W.beta[b];
-        const bool first = W.it[b] == 0;
-        const double* rr = V.r + (size_t)b * L.ld;
-        const double* po = p_old + (size_t)b * L.ld;
-        double* sp = smem + (size_t)c * span;
-        for (int base = lo + 2 * threadIdx.x; base < hi; base += 2 * PG_DIA_NT * 4) {
-            double2 rv[4], pv[4], dv[8];
+    int bv[C];
+    bool firstv[C];
+    double cbv[C], betav[C];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int j = base + 2 * PG_DIA_NT * k;
-                if (j < hi) {
-                    rv[k] = ld2(rr + j);
-                    pv[k] = first ? make_double2(0.0, 0.0) : ld2(po + j);
-                    dv[2 * k] = j < L.n ? __ldg(L.mk + j) : make_double2(1.0, 1.0);
-                    dv[2 * k + 1] = j + 1 < L.n ? __ldg(L.mk + j + 1) : make_double2(1.0, 1.0);
-                }
-            }
+    for (int c = 0; c < C; ++c) {
+        bv[c] = c < nc ? W.act[cur][slot0 + c] : 0;
+        firstv[c] = W.it[bv[c]] == 0;
+        cbv[c] = inv_dt[bv[c]];
+        betav[c] = W.beta[bv[c]];
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+        uint32_t tx = 0;
+        const uint32_t bytes = (uint32_t)span * 8u;
+        for (int c = 0; c < nc; ++c) tx += firstv[c] ? bytes : 2u * bytes;
+        mbar_arrive_expect_tx(&bar, tx);
+        for (int c = 0; c < nc; ++c) {
+            double* sr = smem + (size_t)c * 2 * SPAN;
+            tma_load_1d(sr, V.r + (size_t)bv[c] * L.ld + lo, bytes, &bar);
+            if (!firstv[c])
+                tma_load_1d(sr + SPAN, p_old + (size_t)bv[c] * L.ld + lo, bytes, &bar);
+        }
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    // p_new over the halo, in place (column-major loop so D^-1 loads are shared)
+    for (int jj = 2 * threadIdx.x; jj < span; jj += 2 * PG_DIA_NT) {
+        const int j = lo + jj;
+        const double2 d0 = j < L.n ? __ldg(L.mk + j) : make_double2(1.0, 1.0);
+        const double2 d1 = j + 1 < L.n ? __ldg(L.mk + j + 1) : make_double2(1.0, 1.0);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int j = base + 2 * PG_DIA_NT * k;
-                if (j < hi) {
-                    const double z0 = rv[k].x * dinv_of(cb, dv[2 * k].x, dv[2 * k].y);
-                    const double z1 = rv[k].y * dinv_of(cb, dv[2 * k + 1].x, dv[2 * k + 1].y);
-                    double2 o;
-                    o.x = first ? z0 : fma(beta, pv[k].x, z0);
-                    o.y = first ? z1 : fma(beta, pv[k].y, z1);
-                    *reinterpret_cast<double2*>(sp + j - lo) = o;
-                }
+        for (int c = 0; c < C; ++c) {
+            if (c >= nc) break;
+            double* sr = smem + (size_t)c * 2 * SPAN;
+            double* sp = sr + SPAN;
+            const double2 rv = *reinterpret_cast<const double2*>(sr + jj);
+            double2 o;
+            o.x = rv.x * dinv_of(cbv[c], d0.x, d0.y);
+            o.y = rv.y * dinv_of(cbv[c], d1.x, d1.y);
+            if (!firstv[c]) {
+                const double2 pv = *reinterpret_cast<const double2*>(sp + jj);
+                o.x = fma(betav[c], pv.x, o.x);
+                o.y = fma(betav[c], pv.y, o.y);
             }
+            *reinterpret_cast<double2*>(sp + jj) = o;
         }
     }
     __syncthreads();
     double pq[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) pq[c] = 0.0;
-    double cbv[C];
-    int bv[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-        bv[c] = c < nc ? W.act[cur][slot0 + c] : 0;
-        cbv[c] = inv_dt[bv[c]];
-    }
     for (int i = r0 + threadIdx.x; i < r1; i += PG_DIA_NT) {
         double2 dg, up[UU], lw[UU];
         dia_load_row<UU>(L, i, dg, up, lw);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if (c >= nc) break;
-            const double* sp = smem + (size_t)c * span - lo;
-            const double q = dia_row<UU>(L, i, cbv[c], sp, &dg, up, lw);
-            const double pi = sp[i];
+            const double* spw = smem + (size_t)c * 2 * SPAN + SPAN - lo;
+            const double q = dia_row<UU>(L, i, cbv[c], spw, &dg, up, lw);
+            const double pi = spw[i];
             pq[c] = fma(pi, q, pq[c]);
-            p_new[(size_t)bv[c] * L.ld + i] = pi;
+            const size_t k = (size_t)bv[c] * L.ld + i;
+            p_new[k] = pi;
+            qv[k] = q;
         }
     }
-    for (int c = 0; c < nc; ++c) {
-        const int b = W.act[cur][slot0 + c];
-        double v[1] = {pq[c]};
-        block_sum<1>(v, red);
-        if (threadIdx.x == 0) W.partial[((size_t)b * L.n_tiles + tile) * 3] = v[0];
-        if (column_last(W.cnt, b, L.n_tiles, &s_flag) && threadIdx.x == 0) {
-            double s = 0.0;
+    cta_partial_nt<C, PG_DIA_NT>(pq, red);
+    if (threadIdx.x == 0)
+        for (int c = 0; c < nc; ++c) W.partial[((size_t)bv[c] * L.n_tiles + tile) * 3] = pq[c];
+    // deferred finalize of the columns of this CTA
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        for (int c = 0; c < nc; ++c) {
+            const int b = bv[c];
+            unsigned prev = 0;
+            if (lane == 0) prev = atomicAdd(&W.cnt[b], 1u);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev != (unsigned)(L.n_tiles - 1)) continue;
+            if (lane == 0) W.cnt[b] = 0u;
+            __threadfence();
+            double a = 0.0;
             const double* pp = W.partial + (size_t)b * L.n_tiles * 3;
-            for (int t = 0; t < L.n_tiles; ++t) s += pp[3 * t];
-            if (s > 0.0) {
-                W.alpha[b] = W.rho[b] / s;
-            } else {
-                W.alpha[b] = 0.0;
-                W.flag[b] = COL_BREAKDOWN;
+            for (int t = lane; t < L.n_tiles; t += 32) a += ld_cg(pp + 3 * t);
+            a = warp_sum(a);
+            if (lane == 0) {
+                if (a > 0.0) {
+                    W.alpha[b] = W.rho[b] / a;
+                } else {
+                    W.alpha[b] = 0.0;
+                    W.flag[b] = COL_BREAKDOWN;
+                }
             }
         }
     }
 }
 
-// --- x, r update + r.z, r.r + convergence + compaction --------------------------------
-template <int C, int UU>
-__global__ void __launch_bounds__(PG_DIA_NT, 2)
-k_dia_upd(DiaLevel L, DiaWork V, PcgWork W, int cur, const double* __restrict__ inv_dt,
-          int max_iters) {
-    extern __shared__ double smem[];
-    __shared__ double red[(PG_DIA_NT / 32) * 2];
+// streaming update: grid (n_chunks, active slots)
+#define PG_UPD_NT 256
+#define PG_UPD_V 4          // double2 per thread per array -> 2048 rows / CTA
+template <int UU>
+__global__ void __launch_bounds__(PG_UPD_NT)
+k_supd(DiaLevel L, DiaWork V, PcgWork W, const double* __restrict__ qv, int cur,
+       const double* __restrict__ inv_dt, int max_iters, int n_chunks) {
+    __shared__ double red[(PG_UPD_NT / 32) * 2];
     __shared__ int s_flag;
-    __shared__ int s_scan[PG_DIA_NT + 1];
+    __shared__ int s_scan[PG_UPD_NT + 1];
     const int na = W.nact[cur];
-    const int slot0 = blockIdx.y * C;
-    const int tile = blockIdx.x;
-    if (slot0 < na) {
-        int r0, r1, lo, hi;
-        tile_span(L, tile, r0, r1, lo, hi);
-        const int span = hi - lo;
-        const double* __restrict__ p = V.p[cur ^ 1];
-        const int nc = min(C, na - slot0);
-        for (int c = 0; c < nc; ++c) {
-            const int b = W.act[cur][slot0 + c];
-            const double* pc = p + (size_t)b * L.ld;
-            double* sp = smem + (size_t)c * span;
-            for (int base = lo + 2 * threadIdx.x; base < hi; base += 2 * PG_DIA_NT * 4) {
-                double2 v[4];
+    const int slot = blockIdx.y;
+    const int chunk = blockIdx.x;
+    if (slot < na) {
+        const int b = W.act[cur][slot];
+        const double cb = inv_dt[b];
+        const double al = W.alpha[b];
+        const size_t base = (size_t)b * L.ld;
+        const double* __restrict__ p = V.p[cur ^ 1] + base;
+        const double* __restrict__ q = qv + base;
+        double* __restrict__ x = V.x + base;
+        double* __restrict__ r = V.r + base;
+        const int i0 = chunk * (PG_UPD_NT * PG_UPD_V * 2);
+        double2 xv[PG_UPD_V], rv[PG_UPD_V], pv[PG_UPD_V], qq[PG_UPD_V];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int j = base + 2 * PG_DIA_NT * k;
-                    if (j < hi) v[k] = ld2(pc + j);
-                }
+        for (int k = 0; k < PG_UPD_V; ++k) {
+            const int i = i0 + 2 * (threadIdx.x + k * PG_UPD_NT);
+            if (i < L.n) {
+                xv[k] = ld2(x + i);
+                rv[k] = ld2(r + i);
+                pv[k] = ld2(p + i);
+                qq[k] = ld2(q + i);
+            }
+        }
+        double acc[2] = {0.0, 0.0};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int j = base + 2 * PG_DIA_NT * k;
-                    if (j < hi) *reinterpret_cast<double2*>(sp + j - lo) = v[k];
+        for (int k = 0; k < PG_UPD_V; ++k) {
+            const int i = i0 + 2 * (threadIdx.x + k * PG_UPD_NT);
+            if (i < L.n) {
+                const double2 d0 = __ldg(L.mk + i);
+                const double2 d1 = (i + 1 < L.n) ? __ldg(L.mk + i + 1) : make_double2(1.0, 1.0);
+                double2 xo, ro;
+                xo.x = fma(al, pv[k].x, xv[k].x);
+                xo.y = fma(al, pv[k].y, xv[k].y);
+                ro.x = fma(-al, qq[k].x, rv[k].x);
+                ro.y = fma(-al, qq[k].y, rv[k].y);   // padding rows: q = r = 0
+                *reinterpret_cast<double2*>(x + i) = xo;
+                *reinterpret_cast<double2*>(r + i) = ro;
+                acc[0] = fma(ro.x * ro.x, dinv_of(cb, d0.x, d0.y), acc[0]);
+                acc[1] = fma(ro.x, ro.x, acc[1]);
+                if (i + 1 < L.n) {
+                    acc[0] = fma(ro.y * ro.y, dinv_of(cb, d1.x, d1.y), acc[0]);
+                    acc[1] = fma(ro.y, ro.y, acc[1]);
                 }
             }
+        }
+        cta_partial_nt<2, PG_UPD_NT>(acc, red);
+        if (threadIdx.x == 0) {
+            double* pp = W.partial + ((size_t)b * n_chunks + chunk) * 3;
+            pp[1] = acc[0]; pp[2] = acc[1];
         }
         __syncthreads();
-        double acc[C][2];
-        double cbv[C], alv[C];
-        int bv[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            acc[c][0] = acc[c][1] = 0.0;
-            bv[c] = c < nc ? W.act[cur][slot0 + c] : 0;
-            cbv[c] = inv_dt[bv[c]];
-            alv[c] = W.alpha[bv[c]];
-        }
-        for (int i = r0 + threadIdx.x; i < r1; i += PG_DIA_NT) {
-            double2 dg, up[UU], lw[UU];
-            dia_load_row<UU>(L, i, dg, up, lw);
-            double xv[C], rv[C];
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                if (c < nc) {
-                    xv[c] = V.x[(size_t)bv[c] * L.ld + i];
-                    rv[c] = V.r[(size_t)bv[c] * L.ld + i];
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                if (c >= nc) break;
-                const double* sp = smem + (size_t)c * span - lo;
-                const double q = dia_row<UU>(L, i, cbv[c], sp, &dg, up, lw);
-                const double pi = sp[i];
-                const size_t k = (size_t)bv[c] * L.ld + i;
-                V.x[k] = fma(alv[c], pi, xv[c]);
-                const double ri = fma(-alv[c], q, rv[c]);
-                V.r[k] = ri;
-                acc[c][0] = fma(ri * ri, dinv_of(cbv[c], dg.x, dg.y), acc[c][0]);
-                acc[c][1] = fma(ri, ri, acc[c][1]);
-            }
-        }
-        for (int c = 0; c < nc; ++c) {
-            const int b = bv[c];
-            double v[2] = {acc[c][0], acc[c][1]};
-            block_sum<2>(v, red);
-            if (threadIdx.x == 0) {
-                double* pp = W.partial + ((size_t)b * L.n_tiles + tile) * 3;
-                pp[1] = v[0]; pp[2] = v[1];
-            }
-            if (column_last(W.cnt, b, L.n_tiles, &s_flag) && threadIdx.x == 0) {
+        if (threadIdx.x == 0) __threadfence();
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            unsigned prev = 0;
+            if (lane == 0) prev = atomicAdd(&W.cnt[b], 1u);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev == (unsigned)(n_chunks - 1)) {
+                if (lane == 0) W.cnt[b] = 0u;
+                __threadfence();
                 double rz = 0.0, rr = 0.0;
-                const double* pp = W.partial + (size_t)b * L.n_tiles * 3;
-                for (int t = 0; t < L.n_tiles; ++t) { rz += pp[3 * t + 1]; rr += pp[3 * t + 2]; }
-                const int it = W.it[b] + 1;
-                W.it[b] = it;
-                W.beta[b] = rz / W.rho[b];
-                W.rho[b] = rz;
-                atomicAdd(W.iters, 1ull);
-                atomicAdd(W.iters + 1, 1ull);
-                atomicMax(W.ictr, it);
-                if (W.flag[b] == COL_ACTIVE) {
-                    if (rr <= W.tol2[b] || rr == 0.0) W.flag[b] = COL_CONVERGED;
-                    else if (it >= max_iters) {
-                        W.flag[b] = COL_MAXIT;
-                        atomicAdd(W.ictr + 1, 1);
-                        atomicAdd(W.ictr + 2, 1);
+                const double* pp = W.partial + (size_t)b * n_chunks * 3;
+                for (int t = lane; t < n_chunks; t += 32) {
+                    rz += ld_cg(pp + 3 * t + 1);
+                    rr += ld_cg(pp + 3 * t + 2);
+                }
+                rz = warp_sum(rz);
+                rr = warp_sum(rr);
+                if (lane == 0) {
+                    const int it = W.it[b] + 1;
+                    W.it[b] = it;
+                    W.beta[b] = rz / W.rho[b];
+                    W.rho[b] = rz;
+                    atomicAdd(W.iters, 1ull);
+                    atomicAdd(W.iters + 1, 1ull);
+                    atomicMax(W.ictr, it);
+                    if (W.flag[b] == COL_ACTIVE) {
+                        if (rr <= W.tol2[b] || rr == 0.0) W.flag[b] = COL_CONVERGED;
+                        else if (it >= max_iters) {
+                            W.flag[b] = COL_MAXIT;
+                            atomicAdd(W.ictr + 1, 1);
+                            atomicAdd(W.ictr + 2, 1);
+                        }
                     }
                 }
             }

@@ -38,6 +38,7 @@ struct Level {
     int off[PG_DIA_MAX + 1] = {0};
     double2* mk = nullptr;
     DiaWork V{};
+    double* qv = nullptr;          // q = A p of the DIA path [B][ld]
     // nonlinear iron elements
     int n_elem = 0;
     int* elem_dof = nullptr;
@@ -306,8 +307,8 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
                 for (int u = 0; u < U; ++u) L.off[u + 1] = offs[u];
                 L.ld = (d->n + 31) & ~31;
                 const int span = L.R + 2 * L.omax + 4;
-                L.Cd = 4;
-                while (L.Cd > 1 && (size_t)L.Cd * span * 8 > 72 * 1024) L.Cd >>= 1;
+                L.Cd = 4;                 // 2 halo arrays per column, <= 72 KB / CTA
+                while (L.Cd > 1 && (size_t)L.Cd * 2 * span * 8 > 72 * 1024) L.Cd >>= 1;
                 if ((size_t)span * 8 > 200 * 1024 || U == 0) L.dia = false;
                 if (L.dia) {
                     int rc0 = dev_upload(ctx, &L.mk, mk.data(), mk.size());
@@ -368,8 +369,10 @@ static int ensure_ws(pg_ctx* ctx, Level& L, int B) {
     if (L.dia && !L.resident) {
         const size_t vld = (size_t)B * L.ld * sizeof(double);
         if ((rc = alloc((void**)&L.V.x, vld)) || (rc = alloc((void**)&L.V.r, vld)) ||
-            (rc = alloc((void**)&L.V.p[0], vld)) || (rc = alloc((void**)&L.V.p[1], vld)))
+            (rc = alloc((void**)&L.V.p[0], vld)) || (rc = alloc((void**)&L.V.p[1], vld)) ||
+            (rc = alloc((void**)&L.qv, vld)))
             return rc;
+        CU(cudaMemset(L.qv, 0, vld));
         // padding rows [n, ld) stay zero forever (kernels write rows < n only)
         CU(cudaMemset(L.V.x, 0, vld));
         CU(cudaMemset(L.V.r, 0, vld));
@@ -384,7 +387,8 @@ static int ensure_ws(pg_ctx* ctx, Level& L, int B) {
         (rc = alloc((void**)&W.beta, B * 8)) || (rc = alloc((void**)&W.tol2, B * 8)) ||
         (rc = alloc((void**)&W.bnorm2, B * 8)) || (rc = alloc((void**)&W.it, B * 4)) ||
         (rc = alloc((void**)&W.flag, B * 4)) ||
-        (rc = alloc((void**)&W.partial, (size_t)B * L.n_tiles * 3 * 8)) ||
+        (rc = alloc((void**)&W.partial,
+                    (size_t)B * std::max(L.n_tiles, L.n / 2048 + 1) * 3 * 8)) ||
         (rc = alloc((void**)&W.cnt, B * 4)) || (rc = alloc((void**)&W.gcnt, 8)) ||
         (rc = alloc((void**)&W.act[0], B * 4)) || (rc = alloc((void**)&W.act[1], B * 4)) ||
         (rc = alloc((void**)&W.nact, 8)))
@@ -497,43 +501,44 @@ static DiaLevel dia_view(const Level& L) {
 }
 
 template <int C, int UU>
-static int launch_dia_iter(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv_dt,
-                           cudaStream_t st) {
-    dim3 grid(L.n_tiles, ny);
-    const size_t sm = (size_t)C * (L.R + 2 * L.omax + 4) * sizeof(double);
+static int launch_dia_iter_c(pg_ctx* ctx, Level& L, int na, int cur, const double* inv_dt,
+                             cudaStream_t st) {
+    const int SPAN = (L.R + 2 * L.omax + 4) & ~1;
+    const size_t sm = (size_t)C * 2 * SPAN * sizeof(double);
     static bool attr_done = false;
     if (!attr_done) {
-        CU(cudaFuncSetAttribute(k_dia_dir<C, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                200 * 1024));
-        CU(cudaFuncSetAttribute(k_dia_upd<C, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CU(cudaFuncSetAttribute(k_sdir<C, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 200 * 1024));
         attr_done = true;
     }
-    k_dia_dir<C, UU><<<grid, PG_DIA_NT, sm, st>>>(dia_view(L), L.V, L.W, cur, inv_dt);
+    dim3 gd(L.n_tiles, (na + C - 1) / C);
+    k_sdir<C, UU><<<gd, PG_DIA_NT, sm, st>>>(dia_view(L), L.V, L.W, L.qv, cur, inv_dt, SPAN);
     LAUNCHED();
-    k_dia_upd<C, UU><<<grid, PG_DIA_NT, sm, st>>>(dia_view(L), L.V, L.W, cur, inv_dt,
-                                                   ctx->opts.max_iters);
+    const int n_chunks = (L.n + PG_UPD_NT * PG_UPD_V * 2 - 1) / (PG_UPD_NT * PG_UPD_V * 2);
+    dim3 gu(n_chunks, na);
+    k_supd<UU><<<gu, PG_UPD_NT, 0, st>>>(dia_view(L), L.V, L.W, L.qv, cur, inv_dt,
+                                          ctx->opts.max_iters, n_chunks);
     LAUNCHED();
     return PG_OK;
 }
 
 template <int UU>
-static int dia_iter_u(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv_dt,
-                      cudaStream_t st) {
+static int launch_dia_iter(pg_ctx* ctx, Level& L, int na, int cur, const double* inv_dt,
+                           cudaStream_t st) {
     switch (L.Cd) {
-        case 4: return launch_dia_iter<4, UU>(ctx, L, ny, cur, inv_dt, st);
-        case 2: return launch_dia_iter<2, UU>(ctx, L, ny, cur, inv_dt, st);
-        default: return launch_dia_iter<1, UU>(ctx, L, ny, cur, inv_dt, st);
+        case 4: return launch_dia_iter_c<4, UU>(ctx, L, na, cur, inv_dt, st);
+        case 2: return launch_dia_iter_c<2, UU>(ctx, L, na, cur, inv_dt, st);
+        default: return launch_dia_iter_c<1, UU>(ctx, L, na, cur, inv_dt, st);
     }
 }
 
-static int dia_iter(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv_dt,
+static int dia_iter(pg_ctx* ctx, Level& L, int na, int cur, const double* inv_dt,
                     cudaStream_t st) {
     switch (L.U) {
-        case 1: return dia_iter_u<1>(ctx, L, ny, cur, inv_dt, st);
-        case 2: return dia_iter_u<2>(ctx, L, ny, cur, inv_dt, st);
-        case 3: return dia_iter_u<3>(ctx, L, ny, cur, inv_dt, st);
-        default: return dia_iter_u<4>(ctx, L, ny, cur, inv_dt, st);
+        case 1: return launch_dia_iter<1>(ctx, L, na, cur, inv_dt, st);
+        case 2: return launch_dia_iter<2>(ctx, L, na, cur, inv_dt, st);
+        case 3: return launch_dia_iter<3>(ctx, L, na, cur, inv_dt, st);
+        default: return launch_dia_iter<4>(ctx, L, na, cur, inv_dt, st);
     }
 }
 
@@ -566,9 +571,8 @@ static int pcg_dia(pg_ctx* ctx, Level& L, int B, const double* u_prev, const dou
     const int K = ctx->opts.check_every;
     if ((rc = poll_nact(ctx, L.W, 0, st, &na))) return rc;
     while (na > 0 && it < ctx->opts.max_iters) {
-        const int ny = (na + L.Cd - 1) / L.Cd;
         for (int k = 0; k < K && it < ctx->opts.max_iters; ++k, ++it) {
-            rc = dia_iter(ctx, L, ny, cur, inv_dt, st);
+            rc = dia_iter(ctx, L, na, cur, inv_dt, st);
             if (rc) return rc;
             cur ^= 1;
         }
