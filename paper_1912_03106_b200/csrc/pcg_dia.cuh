@@ -399,7 +399,7 @@ k_sdir(DiaLevel L, DiaWork V, PcgWork W, double* __restrict__ qv, int cur,
 #define PG_UPD_NT 256
 #define PG_UPD_V 4          // double2 per thread per array -> 2048 rows / CTA
 template <int UU>
-__global__ void __launch_bounds__(PG_UPD_NT)
+__global__ void __launch_bounds__(PG_UPD_NT, 3)
 k_supd(DiaLevel L, DiaWork V, PcgWork W, const double* __restrict__ qv, int cur,
        const double* __restrict__ inv_dt, int max_iters, int n_chunks) {
     __shared__ double red[(PG_UPD_NT / 32) * 2];

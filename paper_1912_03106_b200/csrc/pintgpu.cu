@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -388,7 +389,7 @@ static int ensure_ws(pg_ctx* ctx, Level& L, int B) {
         (rc = alloc((void**)&W.bnorm2, B * 8)) || (rc = alloc((void**)&W.it, B * 4)) ||
         (rc = alloc((void**)&W.flag, B * 4)) ||
         (rc = alloc((void**)&W.partial,
-                    (size_t)B * std::max(L.n_tiles, L.n / 2048 + 1) * 3 * 8)) ||
+                    (size_t)B * std::max(L.n_tiles, L.n / 1024 + 2) * 3 * 8)) ||
         (rc = alloc((void**)&W.cnt, B * 4)) || (rc = alloc((void**)&W.gcnt, 8)) ||
         (rc = alloc((void**)&W.act[0], B * 4)) || (rc = alloc((void**)&W.act[1], B * 4)) ||
         (rc = alloc((void**)&W.nact, 8)))
