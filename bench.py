@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark: MGRIT time-to-solution / fine time-step*DOF/s (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One "step" = one complete MGRIT solve (residual-norm stop at 1e-7) of the
+headline workload, BASELINE config 2 (BASELINE.json configs[1]): 2D P1
+eddy-current model on a 128 x 128 grid (16,129 DOFs), three-phase PWM,
+2^14 implicit-Euler steps on [0, 0.02] s, 3-level V-cycle, FCF, m = 16.
+Spatial coarsening is applied on the coarsest level ("delayed", 2 grids):
+the literal direct 3-grid coarsening stalls in the reference's own algorithm
+on this model (tests/golden/mgrit_cfg2_direct_n32.npz).
+
+value  : whole-job fine time-step*DOF/s = n_steps * n_dofs * K / t, inputs
+         (problem data) resident in HBM, CUDA events on the launch stream,
+         barrier + synchronize on both sides, max over ranks.
+e2e    : the same metric through the public API from host data: problem
+         construction (host assembly, H2D of the level data and excitation
+         tables) + mgrit_solve(gather_solution=True) + D2H of the trajectory.
+roofline: the dominant kernel of the solve (streamed Jacobi-PCG), algorithmic
+         bytes per launch / CUDA-event launch duration, vs MEASURED_PEAKS.json.
+cpu_baseline: the CPU oracle port (oracle/, reference algorithm restated:
+         reference MGRIT engine order + banded Cholesky Phi) on a bounded
+         window of the same workload, one core.
+--impl reference: the oracle port on all host cores (independent windows in
+         parallel processes), same metric; rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HEADLINE = dict(N=128, n_steps=2 ** 14, levels=3, grids=2, strategy="delayed")
+CPU_WINDOW_STEPS = 256          # bounded CPU sample: first 256 fine steps (same dt)
+
+
+def headline_spec(**over):
+    from paper_1912_03106_b200 import configs
+    kw = dict(HEADLINE)
+    kw.update(over)
+    return configs.config2(**kw)
+
+
+def workload_config(spec, world):
+    mg = spec["mgrit"]
+    return {
+        "workload": "BASELINE config 2 (configs[1]): linear 2D P1 eddy-current, 3-phase PWM, "
+                    "MGRIT V(FCF) 3 levels m=16, spatial coarsening on the coarsest level",
+        "mesh": f"{spec['N']}x{spec['N']} cells, {(spec['N'] - 1) ** 2} DOFs",
+        "n_steps": spec["n_steps"],
+        "levels": len(mg["factors"]) + 1,
+        "m": mg["factors"][0],
+        "spatial_strategy": mg["spatial_strategy"],
+        "n_spatial_grids": spec["n_spatial_grids"],
+        "tolerance": mg["tolerance"],
+        "inner_solver": f"batched Jacobi-PCG rtol {spec['inner']['rtol']}",
+        "parallelism": f"time-parallel C-intervals over {world} GPU(s)",
+        "l2": "working set > L2 (level-0 batch vectors 132 MB each); no flush needed",
+    }
+
+
+# --- clocks ------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.dev), "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+# --- CPU oracle arms ----------------------------------------------------------------
+
+def _oracle_window(n_steps):
+    """Oracle MGRIT on the first n_steps fine steps of the headline workload
+    (same mesh, dt, m, levels); returns (seconds, iterations, n_dofs)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import fem2d, mgrit as om, time_hierarchy as oth
+    spec = headline_spec(n_steps=n_steps)
+    prob = fem2d.make_problem(spec)
+    tf = spec["tf"] * n_steps / HEADLINE["n_steps"]
+    grid = oth.build_uniform_grid(0.0, tf, n_steps)
+    hier = oth.TimeHierarchy.build(grid, spec["mgrit"]["factors"])
+    mg = spec["mgrit"]
+    t0 = time.perf_counter()
+    run, _ = om.mgrit_solve(prob, hier,
+                            om.CycleSpec(kind=mg["kind"], gamma=mg["gamma"],
+                                         spatial_strategy=mg["spatial_strategy"]),
+                            om.StoppingCriterion(tolerance=mg["tolerance"]),
+                            gather_solution=False)
+    return time.perf_counter() - t0, run.iterations, prob.spatial.size(0)
+
+
+def cpu_baseline_single():
+    secs, iters, n = _oracle_window(CPU_WINDOW_STEPS)
+    return {"value": CPU_WINDOW_STEPS * n / secs, "unit": "fine time-step*DOF/s",
+            "cores": 1, "kind": "port",
+            "sample": f"oracle MGRIT (reference engine order, banded-Cholesky Phi) on the first "
+                      f"{CPU_WINDOW_STEPS} fine steps of the workload (same mesh/dt/m/levels), "
+                      f"{iters} iterations, {secs:.1f} s, 1 core"}
+
+
+def _pool_window(_):
+    return _oracle_window(CPU_WINDOW_STEPS)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    ctx = mp.get_context("fork")
+    n = None
+    vals = []
+    with ctx.Pool(cores) as pool:
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_pool_window, range(cores))
+            dt = time.perf_counter() - t0
+            n = res[0][2]
+            if k >= args.warmup:
+                vals.append((dt, res[0][1]))
+    total = sum(v[0] for v in vals)
+    value = args.steps * cores * CPU_WINDOW_STEPS * n / total
+    spec = headline_spec()
+    line = {
+        "metric": "MGRIT time-to-solution as fine time-step*DOF/s", "impl": "reference",
+        "value": value, "unit": "fine time-step*DOF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(spec, 1),
+        "cpu_baseline": {"value": value, "unit": "fine time-step*DOF/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"each step: {cores} independent oracle MGRIT windows of "
+                                   f"{CPU_WINDOW_STEPS} fine steps in {cores} processes "
+                                   f"({vals[0][1]} iterations each)"},
+        "e2e": {"value": value, "unit": "fine time-step*DOF/s",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --- B200 arm ------------------------------------------------------------------------
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1912_03106_b200 import (CycleSpec, DistTransport, GpuFemProblem, MgritSolver,
+                                       NullTransport, StoppingCriterion, TimeHierarchy,
+                                       build, build_uniform_grid, mgrit_solve)
+    build.build()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        transport = DistTransport(device=dev)
+    else:
+        transport = NullTransport()
+    spec = headline_spec()
+    mg = spec["mgrit"]
+    n_steps = spec["n_steps"]
+
+    def make_solver(problem):
+        grid = build_uniform_grid(0.0, spec["tf"], n_steps)
+        hier = TimeHierarchy.build(grid, mg["factors"])
+        return MgritSolver(problem, hier,
+                           CycleSpec(kind=mg["kind"], gamma=mg["gamma"],
+                                     max_iters=mg["max_iters"],
+                                     spatial_strategy=mg["spatial_strategy"]),
+                           StoppingCriterion(tolerance=mg["tolerance"]), transport), hier
+
+    problem = GpuFemProblem(spec, device=local)
+    solver, hier = make_solver(problem)
+    n0 = problem.spatial.size(0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        run, _ = solver.solve(gather_solution=False)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    problem.profile(True)
+    launches0 = problem.launch_count()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    runs = []
+    for _ in range(args.steps):
+        run, _ = solver.solve(gather_solution=False)
+        runs.append(run)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    prof = problem.profile_read(reset=True)
+    problem.profile(False)
+    launches = problem.launch_count() - launches0
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    value = args.steps * n_steps * n0 / elapsed
+
+    # --- end to end through the public API, host data in, host trajectory out
+    barrier()
+    t0 = time.perf_counter()
+    p2 = GpuFemProblem(spec, device=local)
+    h2d = sum(g.row_ptr.nbytes + g.col_idx.nbytes + g.m_val.nbytes + g.k_val.nbytes
+              + g.shapes.nbytes + g.weights.nbytes for g in p2.grids)
+    s2, _ = make_solver(p2)
+    h2d += sum(lv.inv_dt_all.numel() * 8 + sum(t.numel() * 8 for t in lv.src_all)
+               for lv in s2.levels)
+    run2, sol = s2.solve(gather_solution=True)
+    host = sol.cpu().numpy() if sol is not None else None
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    d2h = int(host.nbytes) if host is not None else 0
+    del host, sol
+    p2.close()
+
+    if rank != 0:
+        return 0
+    peak, peak_src = measured_peak()
+    kernels = []
+    for k in prof:
+        if k["launches"]:
+            avg_ms = k["total_ms"] / k["launches"]
+            per_launch = k["alg_bytes"] / k["launches"]
+            kernels.append(dict(name=k["name"], launches=k["launches"],
+                                avg_ms=avg_ms, alg_bytes_per_launch=per_launch,
+                                achieved_gbs=per_launch / (avg_ms * 1e-3) / 1e9,
+                                total_ms=k["total_ms"]))
+    kernels.sort(key=lambda k: -k["total_ms"])
+    roofline = None
+    if kernels:
+        top = kernels[0]
+        tr = ncu_traffic()
+        traffic = None
+        if tr and tr.get("kernel") == top["name"] and tr.get("workload") == "cfg2-headline":
+            traffic = tr.get("dram_bytes_per_launch")
+        pcg_ms = sum(k["total_ms"] for k in kernels)
+        roofline = {"bound": "hbm", "kernel": top["name"], "achieved": top["achieved_gbs"],
+                    "peak": peak, "unit": "GB/s", "frac": top["achieved_gbs"] / peak,
+                    "traffic": traffic, "peak_source": peak_src,
+                    "alg_bytes_model": "k_sdir 32 n, k_supd 48 n bytes per active column",
+                    "kernels": kernels,
+                    "pcg_share_of_step": (pcg_ms / 1e3) / elapsed}
+    cpu = cpu_baseline_single() if world == 1 and not args.no_cpu else None
+    r = runs[-1]
+    line = {
+        "metric": "MGRIT time-to-solution as fine time-step*DOF/s",
+        "value": value, "unit": "fine time-step*DOF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config 2 model, no external data)",
+        "config": workload_config(spec, world),
+        "time_to_solution_s": elapsed / args.steps,
+        "mgrit": {"iterations": r.iterations, "converged": r.converged,
+                  "residual_history": [r.initial_residual] + list(r.residual_norms),
+                  "phi_columns_per_solve": r.phi_columns, "phi_calls_per_solve": r.phi_calls},
+        "e2e": {"value": n_steps * n0 / e2e_s, "unit": "fine time-step*DOF/s",
+                "seconds": e2e_s, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -158,6 +158,20 @@ int  pg_fas_rhs(pg_ctx* ctx, int coarse, int coarsen, int B,
 /* Number of kernels this context has launched (for the bench). */
 int64_t pg_launch_count(pg_ctx* ctx);
 
+/* Kernel-level timing of the streamed PCG (CUDA events around every
+ * k_sdir / k_supd launch, read back at the existing convergence polls).
+ * alg_bytes: algorithmic HBM bytes of those launches (32 n per column for
+ * k_sdir, 48 n for k_supd). */
+typedef struct pg_kernel_profile {
+    char    name[16];
+    double  total_ms;
+    int64_t launches;
+    double  alg_bytes;
+    int64_t column_iters;
+} pg_kernel_profile;
+int  pg_profile(pg_ctx* ctx, int on);
+int  pg_profile_read(pg_ctx* ctx, pg_kernel_profile* out, int n, int reset);
+
 #ifdef __cplusplus
 }
 #endif

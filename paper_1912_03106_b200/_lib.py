@@ -50,6 +50,11 @@ class PhiStats(ctypes.Structure):
     ]
 
 
+class KernelProfile(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 16), ("total_ms", c_double), ("launches", c_int64),
+                ("alg_bytes", c_double), ("column_iters", c_int64)]
+
+
 EXPORTS = {
     "pg_create": (c_int, [ctypes.POINTER(c_void_p), c_int]),
     "pg_destroy": (None, [c_void_p]),
@@ -70,6 +75,8 @@ EXPORTS = {
     "pg_fas_rhs": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,
                            c_void_p, c_void_p, c_int, c_void_p]),
     "pg_launch_count": (c_int64, [c_void_p]),
+    "pg_profile": (c_int, [c_void_p, c_int]),
+    "pg_profile_read": (c_int, [c_void_p, ctypes.POINTER(KernelProfile), c_int, c_int]),
 }
 
 _LIB = None

@@ -70,6 +70,16 @@ struct pg_ctx {
     int* h_poll = nullptr;        // pinned
     int last_level = -1;
     int newton_fail_col = -1, newton_fail_iters = 0;
+    // kernel profiling (CUDA events around every streamed-PCG launch)
+    bool prof_on = false;
+    std::vector<cudaEvent_t> ev;         // pool: [2 per launch] within a poll chunk
+    int ev_used = 0;
+    std::vector<int> ev_kind;            // 0 = k_sdir, 1 = k_supd
+    double prof_ms[2] = {0.0, 0.0};
+    double prof_bytes[2] = {0.0, 0.0};
+    int64_t prof_launches[2] = {0, 0};
+    int64_t prof_cols = 0;
+    unsigned long long prof_iters_seen = 0;
 };
 
 static int set_err(pg_ctx* ctx, int code, const char* fmt, ...) {
@@ -180,6 +190,7 @@ extern "C" void pg_destroy(pg_ctx* ctx) {
     for (auto& L : ctx->levels) free_level(L);
     cudaFree(ctx->d_iters);
     cudaFree(ctx->d_ictr);
+    for (auto e : ctx->ev) cudaEventDestroy(e);
     cudaFreeHost(ctx->h_poll);
     delete ctx;
 }
@@ -501,6 +512,44 @@ static DiaLevel dia_view(const Level& L) {
     return v;
 }
 
+static int prof_mark(pg_ctx* ctx, int kind, cudaStream_t st) {
+    if (!ctx->prof_on) return PG_OK;
+    if (ctx->ev_used + 1 >= (int)ctx->ev.size()) {
+        const int add = 256;
+        for (int k = 0; k < add; ++k) {
+            cudaEvent_t e;
+            CU(cudaEventCreate(&e));
+            ctx->ev.push_back(e);
+        }
+    }
+    CU(cudaEventRecord(ctx->ev[ctx->ev_used], st));
+    ctx->ev_kind.push_back(kind);
+    ctx->ev_used++;
+    return PG_OK;
+}
+
+// after a stream sync: fold recorded (start, end) pairs into the totals
+static int prof_collect(pg_ctx* ctx, const Level& L) {
+    if (!ctx->prof_on) return PG_OK;
+    for (int k = 0; k + 1 < ctx->ev_used; k += 2) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]));
+        const int kind = ctx->ev_kind[k];
+        ctx->prof_ms[kind] += ms;
+        ctx->prof_launches[kind]++;
+    }
+    ctx->ev_used = 0;
+    ctx->ev_kind.clear();
+    unsigned long long it = 0;
+    CU(cudaMemcpy(&it, ctx->d_iters, sizeof it, cudaMemcpyDeviceToHost));
+    const unsigned long long d = it - ctx->prof_iters_seen;
+    ctx->prof_iters_seen = it;
+    ctx->prof_cols += (int64_t)d;
+    ctx->prof_bytes[0] += 32.0 * L.n * (double)d;   // read r, p_old; write p_new, q
+    ctx->prof_bytes[1] += 48.0 * L.n * (double)d;   // read x, r, p, q; write x, r
+    return PG_OK;
+}
+
 template <int C, int UU>
 static int launch_dia_iter_c(pg_ctx* ctx, Level& L, int na, int cur, const double* inv_dt,
                              cudaStream_t st) {
@@ -513,13 +562,18 @@ static int launch_dia_iter_c(pg_ctx* ctx, Level& L, int na, int cur, const doubl
         attr_done = true;
     }
     dim3 gd(L.n_tiles, (na + C - 1) / C);
+    int rc;
+    if ((rc = prof_mark(ctx, 0, st))) return rc;
     k_sdir<C, UU><<<gd, PG_DIA_NT, sm, st>>>(dia_view(L), L.V, L.W, L.qv, cur, inv_dt, SPAN);
     LAUNCHED();
+    if ((rc = prof_mark(ctx, 0, st))) return rc;
     const int n_chunks = (L.n + PG_UPD_NT * PG_UPD_V * 2 - 1) / (PG_UPD_NT * PG_UPD_V * 2);
     dim3 gu(n_chunks, na);
+    if ((rc = prof_mark(ctx, 1, st))) return rc;
     k_supd<UU><<<gu, PG_UPD_NT, 0, st>>>(dia_view(L), L.V, L.W, L.qv, cur, inv_dt,
                                           ctx->opts.max_iters, n_chunks);
     LAUNCHED();
+    if ((rc = prof_mark(ctx, 1, st))) return rc;
     return PG_OK;
 }
 
@@ -578,6 +632,7 @@ static int pcg_dia(pg_ctx* ctx, Level& L, int B, const double* u_prev, const dou
             cur ^= 1;
         }
         if ((rc = poll_nact(ctx, L.W, cur, st, &na))) return rc;
+        if ((rc = prof_collect(ctx, L))) return rc;
     }
     dim3 grid(std::max(1, std::min(64, (L.n + 255) / 256)), B);
     k_dia_finish<<<grid, 256, 0, st>>>(L.n, L.ld, B, L.V.x, u_out, g, g_idx);
@@ -792,3 +847,35 @@ extern "C" int pg_fas_rhs(pg_ctx* ctx, int coarse, int coarsen, int B, const dou
 #include "newton_host.inc"
 
 extern "C" int64_t pg_launch_count(pg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" int pg_profile(pg_ctx* ctx, int on) {
+    if (!ctx) return PG_EINVAL;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaDeviceSynchronize());
+    unsigned long long it = 0;
+    CU(cudaMemcpy(&it, ctx->d_iters, sizeof it, cudaMemcpyDeviceToHost));
+    ctx->prof_iters_seen = it;
+    ctx->ev_used = 0;
+    ctx->ev_kind.clear();
+    ctx->prof_on = on != 0;
+    return PG_OK;
+}
+
+extern "C" int pg_profile_read(pg_ctx* ctx, pg_kernel_profile* out, int n, int reset) {
+    if (!ctx || !out || n < 2) return PG_EINVAL;
+    const char* names[2] = {"k_sdir", "k_supd"};
+    for (int k = 0; k < 2; ++k) {
+        snprintf(out[k].name, sizeof out[k].name, "%s", names[k]);
+        out[k].total_ms = ctx->prof_ms[k];
+        out[k].launches = ctx->prof_launches[k];
+        out[k].alg_bytes = ctx->prof_bytes[k];
+        out[k].column_iters = ctx->prof_cols;
+    }
+    if (reset) {
+        ctx->prof_ms[0] = ctx->prof_ms[1] = 0.0;
+        ctx->prof_bytes[0] = ctx->prof_bytes[1] = 0.0;
+        ctx->prof_launches[0] = ctx->prof_launches[1] = 0;
+        ctx->prof_cols = 0;
+    }
+    return PG_OK;
+}

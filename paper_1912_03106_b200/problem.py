@@ -202,6 +202,16 @@ class GpuFemProblem:
                    "pg_total_stats")
         return {k: int(getattr(s, k)) for k, _ in s._fields_}
 
+    def profile(self, on=True):
+        _lib.check(self.ctx, self.lib.pg_profile(self.ctx, int(bool(on))), "pg_profile")
+
+    def profile_read(self, reset=False):
+        arr = (_lib.KernelProfile * 2)()
+        _lib.check(self.ctx, self.lib.pg_profile_read(self.ctx, arr, 2, int(reset)),
+                   "pg_profile_read")
+        return [dict(name=a.name.decode(), total_ms=a.total_ms, launches=int(a.launches),
+                     alg_bytes=a.alg_bytes, column_iters=int(a.column_iters)) for a in arr]
+
     def launch_count(self):
         return int(self.lib.pg_launch_count(self.ctx))
 
