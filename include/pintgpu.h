@@ -76,7 +76,12 @@ typedef struct pg_level_desc {
 
 /* Inner-solver and material options (NewtonOptions, problems.py:39-50;
  * BrauerCurve, problems.py:149-168, scaled by nu0 for the 2D model). */
+#define PG_INNER_PCG       0   /* batched Jacobi-PCG                       */
+#define PG_INNER_CHOLESKY  1   /* banded Cholesky per distinct dt (the
+                                  reference's cholesky_banded path)        */
+
 typedef struct pg_solver_opts {
+    int32_t inner;              /* PG_INNER_PCG | PG_INNER_CHOLESKY (linear) */
     double  rtol;               /* PCG: |r| <= rtol |b| per column         */
     int32_t max_iters;          /* PCG iteration cap                       */
     int32_t check_every;        /* host convergence poll interval (iters)  */

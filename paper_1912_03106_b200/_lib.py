@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
                         "libpintgpu.so")
 
 PG_OK, PG_EINVAL, PG_ECUDA, PG_ENEWTON, PG_ENOCONV = 0, 1, 2, 3, 4
+PG_INNER_PCG, PG_INNER_CHOLESKY = 0, 1
 
 c_int, c_int32, c_int64, c_double = (ctypes.c_int, ctypes.c_int32,
                                      ctypes.c_int64, ctypes.c_double)
@@ -36,7 +37,7 @@ class LevelDesc(ctypes.Structure):
 
 class SolverOpts(ctypes.Structure):
     _fields_ = [
-        ("rtol", c_double), ("max_iters", c_int32), ("check_every", c_int32),
+        ("inner", c_int32), ("rtol", c_double), ("max_iters", c_int32), ("check_every", c_int32),
         ("newton_tol", c_double), ("newton_max_iters", c_int32),
         ("damping", c_double), ("max_halvings", c_int32),
         ("nu0", c_double), ("k1", c_double), ("k2", c_double), ("k3", c_double),

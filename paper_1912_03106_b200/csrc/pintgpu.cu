@@ -7,6 +7,7 @@
 #include "pcg_dia.cuh"
 #include "mgrit_ops.cuh"
 #include "newton.cuh"
+#include "band.cuh"
 
 #include <algorithm>
 #include <cstdarg>
@@ -14,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 namespace {
@@ -40,6 +42,20 @@ struct Level {
     double2* mk = nullptr;
     DiaWork V{};
     double* qv = nullptr;          // q = A p of the DIA path [B][ld]
+    // banded-Cholesky path (per distinct dt factors)
+    int bw = 0, bwin = 0, LDA = 0, nblk = 0, np = 0;
+    bool band_ok = false;
+    std::unordered_map<uint64_t, int> fac_index;
+    std::vector<double*> FL, FU;
+    double** d_FL = nullptr;
+    double** d_FU = nullptr;
+    int fac_cap = 0;
+    double* Y = nullptr;
+    int Y_B = 0;
+    int* d_perm = nullptr;
+    int4* d_chunks = nullptr;
+    int perm_cap = 0;
+    int* d_status = nullptr;
     // nonlinear iron elements
     int n_elem = 0;
     int* elem_dof = nullptr;
@@ -161,6 +177,7 @@ extern "C" int pg_create(pg_ctx** out, int device) {
     ctx->opts.k1 = 0.0;
     ctx->opts.k2 = 0.0;
     ctx->opts.k3 = 1.0;
+    ctx->opts.inner = PG_INNER_PCG;
     if (cudaMalloc(&ctx->d_iters, 2 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&ctx->d_ictr, 3 * sizeof(int)) != cudaSuccess ||
         cudaMemset(ctx->d_iters, 0, 2 * sizeof(unsigned long long)) != cudaSuccess ||
@@ -176,11 +193,14 @@ extern "C" int pg_create(pg_ctx** out, int device) {
 static void free_level(Level& L) {
     void* ptrs[] = {L.row_ptr, L.col_idx, L.m_val, L.k_val, L.dM, L.dK, L.shapes,
                     L.weights, L.tile_lo, L.tile_hi, L.elem_dof, L.elem_geo,
-                    L.ne_ptr, L.ne, L.mk};
+                    L.ne_ptr, L.ne, L.mk, L.d_FL, L.d_FU, L.Y, L.d_perm, L.d_chunks,
+                    L.d_status};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : L.ws_allocs) cudaFree(p);
     L.ws_allocs.clear();
+    for (double* p : L.FL) cudaFree(p);
+    for (double* p : L.FU) cudaFree(p);
 }
 
 extern "C" void pg_destroy(pg_ctx* ctx) {
@@ -207,6 +227,8 @@ extern "C" int pg_set_options(pg_ctx* ctx, const pg_solver_opts* o) {
         return set_err(ctx, PG_EINVAL, "damping must lie in (0, 1], got %g", o->damping);
     if (o->newton_max_iters < 1 || !(o->newton_tol > 0.0))
         return set_err(ctx, PG_EINVAL, "newton max_iters must be >= 1 and tol positive");
+    if (o->inner != PG_INNER_PCG && o->inner != PG_INNER_CHOLESKY)
+        return set_err(ctx, PG_EINVAL, "inner solver must be PG_INNER_PCG or PG_INNER_CHOLESKY");
     ctx->opts = *o;
     return PG_OK;
 }
@@ -241,6 +263,15 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
         }
     }
     L.resident = d->n <= PG_RES_MAX;
+    // lower bandwidth for the banded-Cholesky path
+    for (int i = 0; i < d->n; ++i)
+        for (int e = d->row_ptr[i]; e < d->row_ptr[i + 1]; ++e)
+            L.bw = std::max(L.bw, i - d->col_idx[e]);
+    L.bwin = std::max(BD_NB, (L.bw + BD_NB - 1) / BD_NB * BD_NB);
+    L.LDA = BD_NB + L.bwin + 4;
+    L.nblk = (d->n + BD_NB - 1) / BD_NB;
+    L.np = L.nblk * BD_NB;
+    L.band_ok = L.bwin <= 256;
     // rows per tile: 1024 (4 rows per thread); halo from the CSR
     L.R = 1024;
     L.n_tiles = (d->n + L.R - 1) / L.R;
@@ -688,6 +719,156 @@ static int newton_batch(pg_ctx* ctx, Level& L, int B, const double* u_prev,
                         const double* guess, const double* inv_dt, const double* src,
                         double* u_out, cudaStream_t st);
 
+// ---------------------------------------------------------------------------
+// banded-Cholesky Phi (problems.py:130-146 on the GPU)
+static int band_solve_bc(const Level& L) { return L.bwin > 128 ? 16 : 32; }
+
+static size_t band_solve_smem(const Level& L) {
+    const int BC = band_solve_bc(L);
+    return (size_t)(2 * BD_NB * L.LDA + (L.bwin / BD_NB) * BD_NB * (BC + 4) + BD_NB * (BC + 4)) *
+           sizeof(double);
+}
+
+static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
+                        cudaStream_t st) {
+    const int nf = (int)cs.size();
+    if (!nf) return PG_OK;
+    const int first = (int)L.FL.size();
+    const size_t fbytes = (size_t)L.nblk * BD_NB * L.LDA * sizeof(double);
+    for (int f = 0; f < nf; ++f) {
+        double *fl = nullptr, *fu = nullptr;
+        CU(cudaMalloc(&fl, fbytes));
+        CU(cudaMalloc(&fu, fbytes));
+        L.FL.push_back(fl);
+        L.FU.push_back(fu);
+    }
+    const int total = (int)L.FL.size();
+    if (total > L.fac_cap) {
+        if (L.d_FL) cudaFree(L.d_FL);
+        if (L.d_FU) cudaFree(L.d_FU);
+        L.fac_cap = std::max(64, 2 * total);
+        CU(cudaMalloc(&L.d_FL, L.fac_cap * sizeof(double*)));
+        CU(cudaMalloc(&L.d_FU, L.fac_cap * sizeof(double*)));
+    }
+    CU(cudaMemcpyAsync(L.d_FL, L.FL.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(L.d_FU, L.FU.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
+    if (!L.d_status) CU(cudaMalloc(&L.d_status, sizeof(int)));
+    CU(cudaMemsetAsync(L.d_status, 0, sizeof(int), st));
+    // scratch lower bands
+    std::vector<double*> lbs(nf);
+    const size_t lbytes = (size_t)L.n * (L.bw + 1) * sizeof(double);
+    for (int f = 0; f < nf; ++f) CU(cudaMallocAsync(&lbs[f], lbytes, st));
+    double** d_lb;
+    double* d_c;
+    CU(cudaMallocAsync(&d_lb, nf * sizeof(double*), st));
+    CU(cudaMallocAsync(&d_c, nf * sizeof(double), st));
+    CU(cudaMemcpyAsync(d_lb, lbs.data(), nf * sizeof(double*), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_c, cs.data(), nf * sizeof(double), cudaMemcpyHostToDevice, st));
+    BandFactorArgs a{L.n, L.bw, L.bwin, L.LDA, L.nblk, L.row_ptr, L.col_idx, L.m_val, L.k_val};
+    dim3 gb(std::min(1024, (L.n + 255) / 256), nf);
+    k_band_build<<<gb, 256, 0, st>>>(a, d_c, d_lb);
+    LAUNCHED();
+    const size_t sm = (size_t)(2 * BD_NB * (BD_NB + 1) + L.bw * (BD_NB + 1)) * sizeof(double);
+    CU(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_band_factor<<<nf, 256, sm, st>>>(a, d_lb, L.d_FL + first, L.d_FU + first, L.d_status);
+    LAUNCHED();
+    for (int f = 0; f < nf; ++f) CU(cudaFreeAsync(lbs[f], st));
+    CU(cudaFreeAsync(d_lb, st));
+    CU(cudaFreeAsync(d_c, st));
+    int status = 0;
+    CU(cudaMemcpyAsync(&status, L.d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (status)
+        return set_err(ctx, PG_EINVAL, "matrix not positive definite (pivot %d)", status - 1);
+    return PG_OK;
+}
+
+static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* inv_dt,
+                    const double* src, double* u_out, const double* g, const int* g_idx,
+                    cudaStream_t st) {
+    std::vector<double> c(B);
+    CU(cudaMemcpyAsync(c.data(), inv_dt, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    // factor index per column (cached per bitwise value of 1/dt, like the
+    // reference's (grid, float(dt)) cache), new factors in one launch
+    std::vector<int> fid(B);
+    std::vector<double> fresh;
+    std::unordered_map<uint64_t, int> pending;
+    for (int b = 0; b < B; ++b) {
+        uint64_t key;
+        memcpy(&key, &c[b], 8);
+        auto it = L.fac_index.find(key);
+        if (it != L.fac_index.end()) { fid[b] = it->second; continue; }
+        auto jt = pending.find(key);
+        if (jt == pending.end()) {
+            const int id = (int)L.FL.size() + (int)fresh.size();
+            pending[key] = id;
+            fresh.push_back(c[b]);
+            fid[b] = id;
+        } else {
+            fid[b] = jt->second;
+        }
+    }
+    int rc = band_factors(ctx, L, fresh, st);
+    if (rc) return rc;
+    for (auto& kv : pending) L.fac_index[kv.first] = kv.second;
+    // group columns by factor -> perm, chunks of BC
+    const int BC = band_solve_bc(L);
+    std::vector<int> perm(B);
+    for (int b = 0; b < B; ++b) perm[b] = b;
+    std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return fid[x] < fid[y]; });
+    std::vector<int4> chunks;
+    for (int i = 0; i < B;) {
+        int j = i;
+        while (j < B && fid[perm[j]] == fid[perm[i]] && j - i < BC) ++j;
+        chunks.push_back(make_int4(fid[perm[i]], i, j - i, 0));
+        i = j;
+    }
+    if (B > L.perm_cap) {
+        if (L.d_perm) cudaFree(L.d_perm);
+        if (L.d_chunks) cudaFree(L.d_chunks);
+        L.perm_cap = std::max(B, 64);
+        CU(cudaMalloc(&L.d_perm, L.perm_cap * sizeof(int)));
+        CU(cudaMalloc(&L.d_chunks, L.perm_cap * sizeof(int4)));
+    }
+    CU(cudaMemcpyAsync(L.d_perm, perm.data(), B * sizeof(int), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(L.d_chunks, chunks.data(), chunks.size() * sizeof(int4),
+                       cudaMemcpyHostToDevice, st));
+    if (B > L.Y_B) {
+        if (L.Y) cudaFree(L.Y);
+        L.Y_B = B;
+        CU(cudaMalloc(&L.Y, (size_t)B * L.np * sizeof(double)));
+    }
+    dim3 gr(std::max(1, std::min(32, (L.np + 255) / 256)), B);
+    k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, L.row_ptr, L.col_idx, L.m_val, L.n_src, L.shapes,
+                                   u_prev, inv_dt, src, L.d_perm, L.Y);
+    LAUNCHED();
+    BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, L.Y, L.d_chunks, L.d_FL};
+    const size_t sm = band_solve_smem(L);
+    const int nch = (int)chunks.size();
+    if (BC == 32) {
+        CU(cudaFuncSetAttribute(k_band_solve<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        CU(cudaFuncSetAttribute(k_band_solve<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_band_solve<32, true><<<nch, BD_NT, sm, st>>>(sa);
+        LAUNCHED();
+        sa.F = L.d_FU;
+        k_band_solve<32, false><<<nch, BD_NT, sm, st>>>(sa);
+        LAUNCHED();
+    } else {
+        CU(cudaFuncSetAttribute(k_band_solve<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        CU(cudaFuncSetAttribute(k_band_solve<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_band_solve<16, true><<<nch, BD_NT, sm, st>>>(sa);
+        LAUNCHED();
+        sa.F = L.d_FU;
+        k_band_solve<16, false><<<nch, BD_NT, sm, st>>>(sa);
+        LAUNCHED();
+    }
+    dim3 gs(std::max(1, std::min(32, (L.n + 255) / 256)), B);
+    k_band_scatter<<<gs, 256, 0, st>>>(L.n, L.np, L.Y, L.d_perm, u_out, g, g_idx);
+    LAUNCHED();
+    return PG_OK;
+}
+
 extern "C" int pg_phi_batch(pg_ctx* ctx, int level, int B, const double* u_prev,
                             const double* guess, const double* inv_dt, const double* src,
                             double* u_out, const double* g, const int32_t* g_idx,
@@ -716,6 +897,8 @@ extern "C" int pg_phi_batch(pg_ctx* ctx, int level, int B, const double* u_prev,
     if (L.n_elem > 0) {
         rc = newton_batch(ctx, L, B, u_prev, guess, inv_dt, src, u_out, st);
         if (rc) return rc;
+    } else if (ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok) {
+        return band_phi(ctx, L, B, u_prev, inv_dt, src, u_out, g, g_idx, st);
     } else if (L.resident) {
         return launch_resident(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st);
     } else if (L.dia) {

@@ -45,7 +45,7 @@ class GpuFemProblem:
     n_scalars = 0
 
     def __init__(self, spec, device=None, rtol=None, max_iters=None,
-                 check_every=16):
+                 check_every=16, inner=None):
         if not torch.cuda.is_available():
             raise PintGpuError("GpuFemProblem needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -69,12 +69,18 @@ class GpuFemProblem:
         self._keep = []
         for g in self.grids:
             self._add_level(g)
-        inner = spec.get("inner", {})
+        inner_cfg = inner_spec = spec.get("inner", {})
         nl = spec.get("nonlinear") or {}
         nt = nl.get("newton", {})
+        kind = inner if inner is not None else inner_cfg.get("kind", "pcg")
+        if kind not in ("pcg", "cholesky"):
+            raise ValueError(f"inner solver must be 'pcg' or 'cholesky', got {kind!r}")
+        self.inner = kind
         self.opts = _lib.SolverOpts(
-            rtol=float(rtol if rtol is not None else inner.get("rtol", 1e-13)),
-            max_iters=int(max_iters if max_iters is not None else inner.get("max_iters", 20000)),
+            inner=_lib.PG_INNER_CHOLESKY if kind == "cholesky" else _lib.PG_INNER_PCG,
+            rtol=float(rtol if rtol is not None else inner_spec.get("rtol", 1e-13)),
+            max_iters=int(max_iters if max_iters is not None
+                          else inner_spec.get("max_iters", 20000)),
             check_every=int(check_every),
             newton_tol=float(nt.get("tol", 1e-11)),
             newton_max_iters=int(nt.get("max_iters", 25)),

@@ -24,28 +24,41 @@ def _run(spec, max_iters, tol, **kw):
     return prob, grid, run, sol
 
 
-@pytest.mark.parametrize("name", ["mgrit_cfg1", "mgrit_cfg2_delayed_n32"])
-def test_mgrit_matches_reference_engine(cuda, name):
-    """Same iteration count; residual history within 1e-8 relative above the
-    Phi noise floor; C-point iterate within 1e-9."""
+# residual-history tolerance per inner solver: banded Cholesky is the
+# reference's algorithm (north-star bar 1e-8 relative); Jacobi-PCG at
+# rtol 1e-13 carries a Phi noise floor of ~1e-13 |u| per C-point that the
+# last (smallest) residuals see at the 1e-7..1e-6 relative level.
+HIST_TOL = {"cholesky": 1e-8, "pcg": 1e-6}
+
+
+@pytest.mark.parametrize("inner", ["cholesky", "pcg"])
+@pytest.mark.parametrize("name", ["mgrit_cfg1", "mgrit_cfg2_delayed_n32",
+                                  "mgrit_cfg2_direct_n32"])
+def test_mgrit_matches_reference_engine(cuda, name, inner):
+    """Same iteration count and residual history as the reference's own
+    engine (mgrit.py) on the same model; C-point iterate within 1e-9."""
     fx = load_golden(name)
-    prob, grid, run, sol = _run(fx["spec"], int(fx["max_iters"]), float(fx["tol"]))
+    prob, grid, run, sol = _run(fx["spec"], int(fx["max_iters"]), float(fx["tol"]),
+                                inner=inner)
     hist = np.array([run.initial_residual] + run.residual_norms)
     ref = fx["history"]
     assert run.iterations == int(fx["iterations"])
     assert run.converged == bool(fx["converged"])
     rel = np.abs(hist - ref) / ref
-    assert rel.max() < 1e-6, rel
+    assert rel.max() < HIST_TOL[inner], rel
+    if "sol_c" not in fx:
+        return
     m = int(fx["factors"][0])
     sol_c = sol.cpu().numpy()[::m]
     err = np.linalg.norm(sol_c - fx["sol_c"]) / np.linalg.norm(fx["sol_c"])
     assert err < 1e-9, err
 
 
-def test_gpu_sequential_matches_reference(cuda):
+@pytest.mark.parametrize("inner", ["cholesky", "pcg"])
+def test_gpu_sequential_matches_reference(cuda, inner):
     fx = load_golden("mgrit_cfg1")
     from paper_1912_03106_b200 import GpuFemProblem, build_uniform_grid, sequential_solve
-    prob = GpuFemProblem(fx["spec"])
+    prob = GpuFemProblem(fx["spec"], inner=inner)
     grid = build_uniform_grid(0.0, fx["spec"]["tf"], fx["spec"]["n_steps"])
     traj = sequential_solve(prob, grid.points).cpu().numpy()
     err = np.linalg.norm(traj[-1] - fx["seq_final"]) / np.linalg.norm(fx["seq_final"])

@@ -13,6 +13,7 @@ PHI_FIXTURES = ["phi_cfg1", "phi_cfg2_n32", "phi_cfg2_n128"]
 
 def _problem(spec, **kw):
     from paper_1912_03106_b200 import GpuFemProblem
+    kw.setdefault("inner", "pcg")
     return GpuFemProblem(spec, **kw)
 
 
@@ -27,20 +28,54 @@ def _phi(prob, g, U, tp, tn, smooth=False, guess=None):
     return out.cpu().numpy(), prob.last_stats()
 
 
+# Tolerances: the banded-Cholesky path is the reference's own algorithm
+# (problems.py:130-146) -> agreement to ~1e-13 relative; Jacobi-PCG stops at
+# |r| <= 1e-13 |b|, whose attainable accuracy is ~kappa * 1e-13 (kappa of
+# the Jacobi-scaled operator ~ 1e3 at 127^2) -> 1e-9.
+TOL = {"cholesky": 1e-12, "pcg": 1e-9}
+
+
+@pytest.mark.parametrize("inner", ["cholesky", "pcg"])
 @pytest.mark.parametrize("name", PHI_FIXTURES)
 @pytest.mark.parametrize("smooth", [False, True])
-def test_phi_batch_matches_oracle(cuda, name, smooth):
-    """Per-column Jacobi-PCG Phi vs the oracle's banded-Cholesky step
-    (problems.py:138-146 restated); tolerance: rtol 1e-13 inner solve ->
-    1e-10 relative per column."""
+def test_phi_batch_matches_oracle(cuda, name, smooth, inner):
+    """Per-column batched Phi vs the oracle's banded-Cholesky step."""
     fx = load_golden(name)
-    prob = _problem(fx["spec"])
+    prob = _problem(fx["spec"], inner=inner)
     for g in range(prob.spatial.n_grids):
         ref = fx[f"phis{g}" if smooth else f"phi{g}"]
         got, st = _phi(prob, g, fx[f"u{g}"], fx[f"tp{g}"], fx[f"tn{g}"], smooth)
         assert st["failed"] == 0
         err = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
-        assert err.max() < 1e-10, (name, g, err.max(), st)
+        assert err.max() < TOL[inner], (name, g, err.max(), st)
+
+
+def test_cholesky_many_dt_and_rhs_add(cuda):
+    """Columns with 5 distinct dt (5 factors, grouped/permuted columns) and
+    the fused g add, vs the oracle."""
+    fx = load_golden("phi_cfg2_n128")
+    from oracle import fem2d
+    prob = _problem(fx["spec"], inner="cholesky")
+    ref = fem2d.make_problem(fx["spec"])
+    n = prob.spatial.size(0)
+    rng = np.random.default_rng(3)
+    B = 37
+    U = rng.standard_normal((B, n)) * 1e-3
+    tn = np.sort(rng.uniform(0.001, 0.02, B))
+    tp = tn - (0.02 / 2 ** 14) * (1 + rng.integers(0, 5, B))
+    dev = prob.device
+    G = torch.randn(4, n, dtype=torch.float64, device=dev)
+    gidx = torch.as_tensor(rng.integers(-1, 4, B).astype(np.int32), device=dev)
+    out = torch.empty(B, n, dtype=torch.float64, device=dev)
+    prob.phi_batch(0, torch.as_tensor(U, device=dev), torch.as_tensor(1.0 / (tn - tp), device=dev),
+                   torch.as_tensor(prob.source_values(tn), device=dev), out, g=G, g_idx=gidx)
+    exp = ref.step_batch(U, tp, tn, 0, False)
+    Gh = G.cpu().numpy()
+    for b, gi in enumerate(gidx.tolist()):
+        if gi >= 0:
+            exp[b] += Gh[gi]
+    err = np.linalg.norm(out.cpu().numpy() - exp, axis=1) / np.linalg.norm(exp, axis=1)
+    assert err.max() < 1e-12, err.max()
 
 
 def test_phi_guess_and_rhs_add(cuda):
@@ -48,7 +83,7 @@ def test_phi_guess_and_rhs_add(cuda):
     prob = _problem(fx["spec"])
     U, tp, tn, ref = fx["u0"], fx["tp0"], fx["tn0"], fx["phi0"]
     got, _ = _phi(prob, 0, U, tp, tn, guess=np.zeros_like(U))
-    assert (np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)).max() < 1e-10
+    assert (np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)).max() < 1e-9
     dev = prob.device
     G = torch.randn(3, U.shape[1], dtype=torch.float64, device=dev)
     gidx = torch.tensor([2, -1, 0, 1], dtype=torch.int32, device=dev)
@@ -60,7 +95,7 @@ def test_phi_guess_and_rhs_add(cuda):
     for b, gi in enumerate(gidx.tolist()):
         if gi >= 0:
             exp[b] += G[gi]
-    assert float((out - exp).abs().max() / exp.abs().max()) < 1e-10
+    assert float((out - exp).abs().max() / exp.abs().max()) < 1e-9
 
 
 def test_step_contract_b1(cuda):
