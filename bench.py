@@ -40,6 +40,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HEADLINE = dict(N=128, n_steps=2 ** 14, levels=3, grids=2, strategy="delayed")
+FP64_NOMINAL_TFLOPS = 40.0      # B200 fp64 / fp64-tensor nominal (no measured fp64 peak)
 CPU_WINDOW_STEPS = 256          # bounded CPU sample: first 256 fine steps (same dt)
 
 
@@ -62,7 +63,9 @@ def workload_config(spec, world):
         "spatial_strategy": mg["spatial_strategy"],
         "n_spatial_grids": spec["n_spatial_grids"],
         "tolerance": mg["tolerance"],
-        "inner_solver": f"batched Jacobi-PCG rtol {spec['inner']['rtol']}",
+        "inner_solver": ("banded Cholesky per distinct dt (reference algorithm), fp64 DMMA solves"
+                         if spec["inner"].get("kind") == "cholesky"
+                         else f"batched Jacobi-PCG rtol {spec['inner']['rtol']}"),
         "parallelism": f"time-parallel C-intervals over {world} GPU(s)",
         "l2": "working set > L2 (level-0 batch vectors 132 MB each); no flush needed",
     }
@@ -215,6 +218,62 @@ def run_reference(args):
 
 # --- B200 arm ------------------------------------------------------------------------
 
+def summarize_kernels(prof, elapsed):
+    out = []
+    for k in prof:
+        if not k["launches"]:
+            continue
+        avg_ms = k["total_ms"] / k["launches"]
+        per_launch = k["alg_bytes"] / k["launches"]
+        d = dict(name=k["name"], launches=k["launches"], avg_ms=avg_ms,
+                 alg_bytes_per_launch=per_launch,
+                 achieved_gbs=per_launch / (avg_ms * 1e-3) / 1e9,
+                 total_ms=k["total_ms"], share_of_step=(k["total_ms"] / 1e3) / elapsed)
+        if k.get("alg_flops"):
+            d["achieved_tflops"] = k["alg_flops"] / (k["total_ms"] * 1e-3) / 1e12
+        out.append(d)
+    out.sort(key=lambda k: -k["total_ms"])
+    return out
+
+
+def phi_microbench(problem_cls, local, peak, B=1024):
+    """BASELINE config 5: one batched Jacobi-PCG Phi (rtol 1e-10) over B
+    N(0,1) states on the 256^2 mesh; CUDA-event kernel timing."""
+    import torch
+    from paper_1912_03106_b200 import configs
+    spec = configs.config5()
+    prob = problem_cls(spec, device=local, inner="pcg")
+    n = prob.spatial.size(0)
+    dev = prob.device
+    U = torch.as_tensor(np.random.default_rng(0).standard_normal((B, n)), device=dev)
+    inv = torch.full((B,), 1.0 / spec["dt"], dtype=torch.float64, device=dev)
+    src = torch.zeros(B, 0, dtype=torch.float64, device=dev)
+    out = torch.empty_like(U)
+    prob.phi_batch(0, U, inv, src, out)              # warm-up
+    torch.cuda.synchronize(dev)
+    prob.profile(True)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    prob.phi_batch(0, U, inv, src, out)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    st = prob.last_stats()
+    t = e0.elapsed_time(e1) / 1e3
+    ks = summarize_kernels(prob.profile_read(reset=True), t)
+    prob.profile(False)
+    alg = st["column_iters"] * 80.0 * n + B * 40.0 * n
+    res = {"workload": "BASELINE config 5: 256x256 (65,025 DOFs), B=1024 N(0,1) states, "
+                       "dt=0.02/2^14, f=0, x0=u_prev, Jacobi-PCG rtol 1e-10",
+           "value": B * n / t, "unit": "time-step*DOF/s", "seconds": t,
+           "batch_iters": st["batch_iters"], "column_iters": st["column_iters"],
+           "alg_bytes": alg, "achieved_gbs": alg / t / 1e9, "frac_of_peak": alg / t / 1e9 / peak,
+           "bytes_model": "80 n per column-iteration (k_sdir 32 n + k_supd 48 n) + 40 n setup",
+           "kernels": ks}
+    prob.close()
+    return res
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -306,16 +365,7 @@ def run_b200(args):
     if rank != 0:
         return 0
     peak, peak_src = measured_peak()
-    kernels = []
-    for k in prof:
-        if k["launches"]:
-            avg_ms = k["total_ms"] / k["launches"]
-            per_launch = k["alg_bytes"] / k["launches"]
-            kernels.append(dict(name=k["name"], launches=k["launches"],
-                                avg_ms=avg_ms, alg_bytes_per_launch=per_launch,
-                                achieved_gbs=per_launch / (avg_ms * 1e-3) / 1e9,
-                                total_ms=k["total_ms"]))
-    kernels.sort(key=lambda k: -k["total_ms"])
+    kernels = summarize_kernels(prof, elapsed)
     roofline = None
     if kernels:
         top = kernels[0]
@@ -323,13 +373,25 @@ def run_b200(args):
         traffic = None
         if tr and tr.get("kernel") == top["name"] and tr.get("workload") == "cfg2-headline":
             traffic = tr.get("dram_bytes_per_launch")
-        pcg_ms = sum(k["total_ms"] for k in kernels)
-        roofline = {"bound": "hbm", "kernel": top["name"], "achieved": top["achieved_gbs"],
-                    "peak": peak, "unit": "GB/s", "frac": top["achieved_gbs"] / peak,
-                    "traffic": traffic, "peak_source": peak_src,
-                    "alg_bytes_model": "k_sdir 32 n, k_supd 48 n bytes per active column",
-                    "kernels": kernels,
-                    "pcg_share_of_step": (pcg_ms / 1e3) / elapsed}
+        if top["name"] == "k_band_solve":
+            roofline = {"bound": "tensor", "kernel": top["name"],
+                        "achieved": top["achieved_tflops"], "peak": FP64_NOMINAL_TFLOPS,
+                        "unit": "TFLOP/s", "frac": top["achieved_tflops"] / FP64_NOMINAL_TFLOPS,
+                        "traffic": traffic,
+                        "peak_source": "nominal B200 fp64 tensor (MEASURED_PEAKS.json has no fp64 "
+                                       "entry)",
+                        "hbm_achieved_gbs": top["achieved_gbs"], "hbm_peak_gbs": peak,
+                        "alg_model": "flops 4 np (W + 32) per column (fwd + bwd); bytes Y in/out "
+                                     "+ each distinct factor once",
+                        "kernels": kernels}
+        else:
+            roofline = {"bound": "hbm", "kernel": top["name"], "achieved": top["achieved_gbs"],
+                        "peak": peak, "unit": "GB/s", "frac": top["achieved_gbs"] / peak,
+                        "traffic": traffic, "peak_source": peak_src,
+                        "alg_model": "k_sdir 32 n, k_supd 48 n bytes per active column",
+                        "kernels": kernels}
+    phi_bench = phi_microbench(problem_cls=GpuFemProblem, local=local, peak=peak) \
+        if not args.no_phi else None
     cpu = cpu_baseline_single() if world == 1 and not args.no_cpu else None
     r = runs[-1]
     line = {
@@ -347,6 +409,7 @@ def run_b200(args):
         "e2e": {"value": n_steps * n0 / e2e_s, "unit": "fine time-step*DOF/s",
                 "seconds": e2e_s, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h},
         "roofline": roofline,
+        "phi_microbench": phi_bench,
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -364,6 +427,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-phi", action="store_true", help="skip the config-5 batched-Phi leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

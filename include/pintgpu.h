@@ -163,15 +163,18 @@ int  pg_fas_rhs(pg_ctx* ctx, int coarse, int coarsen, int B,
 /* Number of kernels this context has launched (for the bench). */
 int64_t pg_launch_count(pg_ctx* ctx);
 
-/* Kernel-level timing of the streamed PCG (CUDA events around every
- * k_sdir / k_supd launch, read back at the existing convergence polls).
- * alg_bytes: algorithmic HBM bytes of those launches (32 n per column for
- * k_sdir, 48 n for k_supd). */
+/* Kernel-level timing (CUDA events around every launch of the hot kernels:
+ * [0] k_sdir, [1] k_supd (streamed PCG, read back at the convergence
+ * polls), [2] k_band_solve (forward + backward banded solves).
+ * alg_bytes: algorithmic HBM bytes (32 n per column for k_sdir, 48 n for
+ * k_supd; Y in/out + distinct factors for the band solves); alg_flops:
+ * 4 np (W + 32) per column for the band solves. */
 typedef struct pg_kernel_profile {
     char    name[16];
     double  total_ms;
     int64_t launches;
     double  alg_bytes;
+    double  alg_flops;
     int64_t column_iters;
 } pg_kernel_profile;
 int  pg_profile(pg_ctx* ctx, int on);

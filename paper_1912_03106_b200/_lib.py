@@ -53,7 +53,7 @@ class PhiStats(ctypes.Structure):
 
 class KernelProfile(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 16), ("total_ms", c_double), ("launches", c_int64),
-                ("alg_bytes", c_double), ("column_iters", c_int64)]
+                ("alg_bytes", c_double), ("alg_flops", c_double), ("column_iters", c_int64)]
 
 
 EXPORTS = {

@@ -47,7 +47,9 @@ _BASE = {
     "mgrit": {"factors": [16], "kind": "V", "gamma": 1, "max_iters": 50,
               "spatial_strategy": "none", "tolerance": 1e-7,
               "nested_iterations": False},
-    "inner": {"rtol": 1e-13, "max_iters": 20000},
+    # inner solve of Phi: "cholesky" = banded Cholesky per distinct dt (the
+    # reference's own cholesky_banded path); "pcg" = batched Jacobi-PCG
+    "inner": {"kind": "cholesky", "rtol": 1e-13, "max_iters": 20000},
 }
 
 
@@ -101,7 +103,7 @@ def config3(N=128, n_steps=2 ** 14, levels=3, carrier="triangle", grids=None,
                       "k3": 3.96e-4,
                       "newton": {"tol": 1e-8, "max_iters": 10, "damping": 0.5,
                                  "max_halvings": 8}}
-    s["inner"]["rtol"] = 1e-12
+    s["inner"].update(kind="pcg", rtol=1e-12)      # config 3: "PCG inner solve"
     s["name"] = "cfg3"
     return s
 
@@ -109,6 +111,7 @@ def config3(N=128, n_steps=2 ** 14, levels=3, carrier="triangle", grids=None,
 def config4(N=512, n_steps=2 ** 16, levels=4, carrier="triangle", grids=None,
             strategy="direct"):
     s = config2(N, n_steps, levels, carrier, grids, strategy)
+    s["inner"]["kind"] = "pcg"        # bandwidth 512: beyond the band-solve smem window
     s["name"] = "cfg4"
     return s
 
@@ -118,7 +121,7 @@ def config5(N=256):
     256^2 mesh, dt = 0.02 / 2^14, f = 0, x0 = u_prev, Jacobi-PCG rtol 1e-10."""
     s = copy.deepcopy(_BASE)
     s.update(N=N, n_steps=2 ** 14)
-    s["inner"] = {"rtol": 1e-10, "max_iters": 20000}
+    s["inner"] = {"kind": "pcg", "rtol": 1e-10, "max_iters": 20000}
     s["dt"] = 0.02 / 2 ** 14
     s["batches"] = [64, 256, 1024, 4096]
     s["name"] = "cfg5"

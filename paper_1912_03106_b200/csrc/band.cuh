@@ -25,7 +25,7 @@
 #include "tma.cuh"
 
 #define BD_NB 32
-#define BD_NT 128          // 4 warps: warp w owns rows 8w..8w+7 of the block
+#define BD_NT 256          // 8 warps: 4 row groups x 2 window halves
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
     asm volatile(
@@ -194,8 +194,12 @@ struct BandSolveArgs {
     double* const* F;            // per factor: FL or FU base
 };
 
-// smem layout (doubles): stage[2][NB * LDA], ring[W/NB][NB][BC + 4], T[NB][BC + 4]
-template <int BC, bool FWD>
+// smem layout (doubles): stage[2][NB * LDA], ring[NSLOT][NB][BC + 4], T[NB][BC + 4]
+// 8 warps: warp w -> row group rg = w & 3 (rows 8 rg .. 8 rg + 7) and window
+// half kh = w >> 2.  The window (NSLOT = W / 32 blocks, a power of two, so
+// ring slots are masks) is fully unrolled; each warp keeps four independent
+// DMMA accumulator chains; the two halves are summed through T.
+template <int BC, int NSLOT, bool FWD>
 __global__ void __launch_bounds__(BD_NT)
 k_band_solve(BandSolveArgs a) {
     extern __shared__ __align__(16) double sm[];
@@ -203,16 +207,20 @@ k_band_solve(BandSolveArgs a) {
     const int4 ch = a.chunks[blockIdx.x];
     const double* F = a.F[ch.x];
     const int col0 = ch.y, ncol = ch.z;
-    constexpr int NB = BD_NB, RS = BC + 4;
-    const int nslot = a.W / NB;
+    constexpr int NB = BD_NB, RS = BC + 4, NT8 = BC / 8;
+    constexpr int W = NSLOT * NB;
+    // per-half window rows: [kh * HALF, kh * HALF + HALF)
+    constexpr int HALF = W / 2;
     double* stage = sm;
     double* ring = stage + 2 * (size_t)NB * a.LDA;
-    double* T = ring + (size_t)nslot * NB * RS;
+    double* T = ring + (size_t)NSLOT * NB * RS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q4 = lane & 3;
+    const int rg = warp & 3, kh = warp >> 2;
+    const int lrow = 8 * rg + g;
     const uint32_t blk_bytes = (uint32_t)(NB * a.LDA * 8);
 
-    for (int t = threadIdx.x; t < nslot * NB * RS; t += BD_NT) ring[t] = 0.0;
+    for (int t = threadIdx.x; t < NSLOT * NB * RS; t += BD_NT) ring[t] = 0.0;
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -224,6 +232,18 @@ k_band_solve(BandSolveArgs a) {
         mbar_arrive_expect_tx(&bar[0], blk_bytes);
         tma_load_1d(stage, F + (size_t)blk_of(0) * NB * a.LDA, blk_bytes, &bar[0]);
     }
+    double nxt[NT8][2];
+    auto load_rhs = [&](int s) {
+        const int rrow = NB * blk_of(s) + lrow;
+#pragma unroll
+        for (int nt = 0; nt < NT8; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cc = 8 * nt + 2 * q4 + h;
+                nxt[nt][h] = (kh == 0 && cc < ncol) ? a.Y[(size_t)(col0 + cc) * a.ldy + rrow] : 0.0;
+            }
+    };
+    load_rhs(0);
     for (int s = 0; s < a.nblk; ++s) {
         const int k = blk_of(s);
         const int st = s & 1;
@@ -233,59 +253,84 @@ k_band_solve(BandSolveArgs a) {
             tma_load_1d(stage + (size_t)(st ^ 1) * NB * a.LDA,
                         F + (size_t)blk_of(s + 1) * NB * a.LDA, blk_bytes, &bar[st ^ 1]);
         }
-        // accumulators: warp rows 8*warp + g, columns 8*nt + 2*q4 + {0,1}
-        double acc[BC / 8][2];
-        const int row = NB * k + 8 * warp + g;
+        double acc[4][NT8][2];
 #pragma unroll
-        for (int nt = 0; nt < BC / 8; ++nt) {
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int cc = 8 * nt + 2 * q4 + h;
-                acc[nt][h] = cc < ncol ? a.Y[(size_t)(col0 + cc) * a.ldy + row] : 0.0;
-            }
+            for (int nt = 0; nt < NT8; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT8; ++nt) {
+            acc[0][nt][0] = nxt[nt][0];
+            acc[0][nt][1] = nxt[nt][1];
         }
+        const int row = NB * k + lrow;
+        if (s + 1 < a.nblk) load_rhs(s + 1);
         mbar_wait(&bar[st], (s >> 1) & 1);
         const double* Lt = stage + (size_t)st * NB * a.LDA;
-        // acc -= Lwin * window ; window row j <-> block (k - nslot + j/NB) (fwd)
-        //                        or (k + 1 + j/NB) (bwd)
-        for (int kk = 0; kk < a.W; kk += 4) {
-            const double av = -Lt[(8 * warp + g) * a.LDA + NB + kk + q4];
-            const int j = kk + q4;
-            const int wb = FWD ? (k - nslot + j / NB) : (k + 1 + j / NB);
-            const bool ok = FWD ? (wb >= 0) : (wb < a.nblk);
-            const double* rr = ring + ((size_t)((wb % nslot + nslot) % nslot) * NB + (j % NB)) * RS;
+        const double* Lrow = Lt + lrow * a.LDA + NB;
+        // window: rows j in [kh*HALF, kh*HALF + HALF); block wbi = j / NB
+        const int kbeg = kh * HALF;
 #pragma unroll
-            for (int nt = 0; nt < BC / 8; ++nt) {
-                const double bv = ok ? rr[8 * nt + g] : 0.0;
-                dmma_8x8x4(acc[nt][0], acc[nt][1], av, bv);
+        for (int jj = 0; jj < HALF; jj += 4) {
+            const int j = kbeg + jj;                    // uniform per warp
+            const int wbi = j / NB;                     // j multiple of 4: exact
+            const int blk = FWD ? (k - NSLOT + wbi) : (k + 1 + wbi);
+            const bool ok = FWD ? (blk >= 0) : (blk < a.nblk);
+            const int slot = (FWD ? (k + wbi) : (k + 1 + wbi)) & (NSLOT - 1);
+            const double av = -Lrow[j + q4];
+            const double* rr = ring + ((size_t)slot * NB + (j % NB) + q4) * RS + g;
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt) {
+                const double bv = ok ? rr[8 * nt] : 0.0;
+                dmma_8x8x4(acc[(jj >> 2) & 3][nt][0], acc[(jj >> 2) & 3][nt][1], av, bv);
             }
         }
-        // T = acc ; y_blk = D^-1 T
+        double r0v[NT8][2];
 #pragma unroll
-        for (int nt = 0; nt < BC / 8; ++nt) {
-            T[(8 * warp + g) * RS + 8 * nt + 2 * q4] = acc[nt][0];
-            T[(8 * warp + g) * RS + 8 * nt + 2 * q4 + 1] = acc[nt][1];
-            acc[nt][0] = acc[nt][1] = 0.0;
+        for (int nt = 0; nt < NT8; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                r0v[nt][h] = (acc[0][nt][h] + acc[1][nt][h]) + (acc[2][nt][h] + acc[3][nt][h]);
+        if (kh == 1) {
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt) {
+                T[lrow * RS + 8 * nt + 2 * q4] = r0v[nt][0];
+                T[lrow * RS + 8 * nt + 2 * q4 + 1] = r0v[nt][1];
+            }
         }
         __syncthreads();
-        for (int kk = 0; kk < NB; kk += 4) {
-            const double av = Lt[(8 * warp + g) * a.LDA + kk + q4];
+        if (kh == 0) {
 #pragma unroll
-            for (int nt = 0; nt < BC / 8; ++nt) {
-                const double bv = T[(kk + q4) * RS + 8 * nt + g];
-                dmma_8x8x4(acc[nt][0], acc[nt][1], av, bv);
+            for (int nt = 0; nt < NT8; ++nt) {
+                T[lrow * RS + 8 * nt + 2 * q4] += r0v[nt][0];
+                T[lrow * RS + 8 * nt + 2 * q4 + 1] += r0v[nt][1];
             }
         }
-        // store into the ring slot of block k and to global
-        double* slot = ring + (size_t)(k % nslot) * NB * RS;
+        __syncthreads();
+        if (kh == 0) {
 #pragma unroll
-        for (int nt = 0; nt < BC / 8; ++nt) {
+            for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int cc = 8 * nt + 2 * q4 + h;
-                slot[(8 * warp + g) * RS + cc] = acc[nt][h];
-                if (cc < ncol) a.Y[(size_t)(col0 + cc) * a.ldy + row] = acc[nt][h];
+                for (int nt = 0; nt < NT8; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
+            const double* Ld = Lt + lrow * a.LDA;
+#pragma unroll
+            for (int kq = 0; kq < NB; kq += 4) {
+                const double av = Ld[kq + q4];
+                const double* tt = T + (kq + q4) * RS + g;
+#pragma unroll
+                for (int nt = 0; nt < NT8; ++nt)
+                    dmma_8x8x4(acc[(kq >> 2) & 3][nt][0], acc[(kq >> 2) & 3][nt][1], av, tt[8 * nt]);
             }
+            double* slot = ring + (size_t)(k & (NSLOT - 1)) * NB * RS;
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cc = 8 * nt + 2 * q4 + h;
+                    const double v = (acc[0][nt][h] + acc[1][nt][h]) + (acc[2][nt][h] + acc[3][nt][h]);
+                    slot[lrow * RS + cc] = v;
+                    if (cc < ncol) a.Y[(size_t)(col0 + cc) * a.ldy + row] = v;
+                }
         }
         __syncthreads();
     }

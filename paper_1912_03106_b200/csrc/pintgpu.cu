@@ -91,9 +91,10 @@ struct pg_ctx {
     std::vector<cudaEvent_t> ev;         // pool: [2 per launch] within a poll chunk
     int ev_used = 0;
     std::vector<int> ev_kind;            // 0 = k_sdir, 1 = k_supd
-    double prof_ms[2] = {0.0, 0.0};
-    double prof_bytes[2] = {0.0, 0.0};
-    int64_t prof_launches[2] = {0, 0};
+    double prof_ms[3] = {0.0, 0.0, 0.0};
+    double prof_bytes[3] = {0.0, 0.0, 0.0};
+    double prof_flops[3] = {0.0, 0.0, 0.0};
+    int64_t prof_launches[3] = {0, 0, 0};
     int64_t prof_cols = 0;
     unsigned long long prof_iters_seen = 0;
 };
@@ -271,7 +272,7 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
     L.LDA = BD_NB + L.bwin + 4;
     L.nblk = (d->n + BD_NB - 1) / BD_NB;
     L.np = L.nblk * BD_NB;
-    L.band_ok = L.bwin <= 256;
+    L.band_ok = (L.bwin == 32 || L.bwin == 64 || L.bwin == 128 || L.bwin == 256);
     // rows per tile: 1024 (4 rows per thread); halo from the CSR
     L.R = 1024;
     L.n_tiles = (d->n + L.R - 1) / L.R;
@@ -721,10 +722,14 @@ static int newton_batch(pg_ctx* ctx, Level& L, int B, const double* u_prev,
 
 // ---------------------------------------------------------------------------
 // banded-Cholesky Phi (problems.py:130-146 on the GPU)
-static int band_solve_bc(const Level& L) { return L.bwin > 128 ? 16 : 32; }
+// columns per solve CTA: 8 (one DMMA n-tile) so a batch of B columns spreads
+// over ~B/8 SMs; 16 when the batch is large enough to fill the GPU anyway.
+static int band_solve_bc(const Level& L, int B, int n_sm) {
+    (void)L;
+    return B >= 16 * n_sm ? 16 : 8;
+}
 
-static size_t band_solve_smem(const Level& L) {
-    const int BC = band_solve_bc(L);
+static size_t band_solve_smem(const Level& L, int BC) {
     return (size_t)(2 * BD_NB * L.LDA + (L.bwin / BD_NB) * BD_NB * (BC + 4) + BD_NB * (BC + 4)) *
            sizeof(double);
 }
@@ -783,6 +788,21 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     return PG_OK;
 }
 
+template <int BC, int NS>
+static int launch_band(pg_ctx* ctx, BandSolveArgs sa, double** d_FU, int nch, size_t sm,
+                       cudaStream_t st) {
+    CU(cudaFuncSetAttribute(k_band_solve<BC, NS, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CU(cudaFuncSetAttribute(k_band_solve<BC, NS, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_band_solve<BC, NS, true><<<nch, BD_NT, sm, st>>>(sa);
+    LAUNCHED();
+    sa.F = d_FU;
+    k_band_solve<BC, NS, false><<<nch, BD_NT, sm, st>>>(sa);
+    LAUNCHED();
+    return PG_OK;
+}
+
 static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* inv_dt,
                     const double* src, double* u_out, const double* g, const int* g_idx,
                     cudaStream_t st) {
@@ -813,7 +833,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     if (rc) return rc;
     for (auto& kv : pending) L.fac_index[kv.first] = kv.second;
     // group columns by factor -> perm, chunks of BC
-    const int BC = band_solve_bc(L);
+    const int BC = band_solve_bc(L, B, ctx->n_sm);
     std::vector<int> perm(B);
     for (int b = 0; b < B; ++b) perm[b] = b;
     std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return fid[x] < fid[y]; });
@@ -844,24 +864,43 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
                                    u_prev, inv_dt, src, L.d_perm, L.Y);
     LAUNCHED();
     BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, L.Y, L.d_chunks, L.d_FL};
-    const size_t sm = band_solve_smem(L);
+    const size_t sm = band_solve_smem(L, BC);
     const int nch = (int)chunks.size();
-    if (BC == 32) {
-        CU(cudaFuncSetAttribute(k_band_solve<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        CU(cudaFuncSetAttribute(k_band_solve<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_band_solve<32, true><<<nch, BD_NT, sm, st>>>(sa);
-        LAUNCHED();
-        sa.F = L.d_FU;
-        k_band_solve<32, false><<<nch, BD_NT, sm, st>>>(sa);
-        LAUNCHED();
-    } else {
-        CU(cudaFuncSetAttribute(k_band_solve<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        CU(cudaFuncSetAttribute(k_band_solve<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_band_solve<16, true><<<nch, BD_NT, sm, st>>>(sa);
-        LAUNCHED();
-        sa.F = L.d_FU;
-        k_band_solve<16, false><<<nch, BD_NT, sm, st>>>(sa);
-        LAUNCHED();
+    if ((rc = prof_mark(ctx, 2, st))) return rc;
+    switch (L.bwin / BD_NB) {
+#define PG_BAND_CASE(NS)                                                                  \
+    case NS:                                                                              \
+        if (BC == 8) rc = launch_band<8, NS>(ctx, sa, L.d_FU, nch, sm, st);              \
+        else rc = launch_band<16, NS>(ctx, sa, L.d_FU, nch, sm, st);                     \
+        break;
+        PG_BAND_CASE(1)
+        PG_BAND_CASE(2)
+        PG_BAND_CASE(4)
+        PG_BAND_CASE(8)
+#undef PG_BAND_CASE
+        default: return set_err(ctx, PG_EINVAL, "band window %d not supported", L.bwin);
+    }
+    if (rc) return rc;
+    if ((rc = prof_mark(ctx, 2, st))) return rc;
+    if (ctx->prof_on) {
+        // algorithmic work of the forward + backward solves: per column
+        // 2 * 2 * np * (W + nb) flops; HBM bytes = Y in/out twice + each
+        // distinct factor pair read once
+        std::vector<char> used(L.FL.size(), 0);
+        for (int b = 0; b < B; ++b) used[fid[b]] = 1;
+        double fb = 0.0;
+        for (char u : used) fb += u ? 2.0 * L.nblk * BD_NB * L.LDA * 8.0 : 0.0;
+        ctx->prof_flops[2] += 4.0 * L.np * (double)(L.bwin + BD_NB) * B;
+        ctx->prof_bytes[2] += 32.0 * L.np * B + fb;
+        CU(cudaStreamSynchronize(st));
+        for (int k = 0; k + 1 < ctx->ev_used; k += 2) {
+            float ms = 0.f;
+            CU(cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]));
+            ctx->prof_ms[ctx->ev_kind[k]] += ms;
+            ctx->prof_launches[ctx->ev_kind[k]] += 2;
+        }
+        ctx->ev_used = 0;
+        ctx->ev_kind.clear();
     }
     dim3 gs(std::max(1, std::min(32, (L.n + 255) / 256)), B);
     k_band_scatter<<<gs, 256, 0, st>>>(L.n, L.np, L.Y, L.d_perm, u_out, g, g_idx);
@@ -1046,18 +1085,20 @@ extern "C" int pg_profile(pg_ctx* ctx, int on) {
 
 extern "C" int pg_profile_read(pg_ctx* ctx, pg_kernel_profile* out, int n, int reset) {
     if (!ctx || !out || n < 2) return PG_EINVAL;
-    const char* names[2] = {"k_sdir", "k_supd"};
-    for (int k = 0; k < 2; ++k) {
+    const char* names[3] = {"k_sdir", "k_supd", "k_band_solve"};
+    for (int k = 0; k < std::min(n, 3); ++k) {
         snprintf(out[k].name, sizeof out[k].name, "%s", names[k]);
         out[k].total_ms = ctx->prof_ms[k];
         out[k].launches = ctx->prof_launches[k];
         out[k].alg_bytes = ctx->prof_bytes[k];
+        out[k].alg_flops = ctx->prof_flops[k];
         out[k].column_iters = ctx->prof_cols;
     }
     if (reset) {
-        ctx->prof_ms[0] = ctx->prof_ms[1] = 0.0;
-        ctx->prof_bytes[0] = ctx->prof_bytes[1] = 0.0;
-        ctx->prof_launches[0] = ctx->prof_launches[1] = 0;
+        for (int k = 0; k < 3; ++k) {
+            ctx->prof_ms[k] = ctx->prof_bytes[k] = ctx->prof_flops[k] = 0.0;
+            ctx->prof_launches[k] = 0;
+        }
         ctx->prof_cols = 0;
     }
     return PG_OK;

@@ -212,11 +212,12 @@ class GpuFemProblem:
         _lib.check(self.ctx, self.lib.pg_profile(self.ctx, int(bool(on))), "pg_profile")
 
     def profile_read(self, reset=False):
-        arr = (_lib.KernelProfile * 2)()
-        _lib.check(self.ctx, self.lib.pg_profile_read(self.ctx, arr, 2, int(reset)),
+        arr = (_lib.KernelProfile * 3)()
+        _lib.check(self.ctx, self.lib.pg_profile_read(self.ctx, arr, 3, int(reset)),
                    "pg_profile_read")
         return [dict(name=a.name.decode(), total_ms=a.total_ms, launches=int(a.launches),
-                     alg_bytes=a.alg_bytes, column_iters=int(a.column_iters)) for a in arr]
+                     alg_bytes=a.alg_bytes, alg_flops=a.alg_flops,
+                     column_iters=int(a.column_iters)) for a in arr]
 
     def launch_count(self):
         return int(self.lib.pg_launch_count(self.ctx))
