@@ -91,7 +91,7 @@ def phi_case(name, spec, B=8, seed=0):
 
 
 def main():
-    which = sys.argv[1:] or ["phi", "cfg1", "cfg2s", "cfg2d", "cfg3s"]
+    which = sys.argv[1:] or ["phi", "cfg1", "cfg2s", "cfg2d", "cfg3s", "variants"]
     if "phi" in which:
         phi_case("phi_cfg2_n32", configs.config2(N=32, n_steps=1024, levels=3))
         s = configs.config2(N=32, n_steps=1024, levels=3)
@@ -114,6 +114,16 @@ def main():
     if "cfg3s" in which:
         s = configs.config3(N=32, n_steps=256, levels=3, grids=2, strategy="delayed")
         mgrit_case("mgrit_cfg3_delayed_n32", s)
+
+
+    if "variants" in which:
+        # F-cycle (mgrit.py:617-626) and nested iterations (mgrit.py:659-675)
+        s = configs.config2(N=32, n_steps=1024, levels=3, grids=2, strategy="delayed")
+        s["mgrit"]["kind"] = "F"
+        mgrit_case("mgrit_cfg2_fcycle_n32", s)
+        s = configs.config2(N=32, n_steps=1024, levels=3, grids=2, strategy="delayed")
+        s["mgrit"]["nested_iterations"] = True
+        mgrit_case("mgrit_cfg2_nested_n32", s)
 
 
 if __name__ == "__main__":

@@ -33,7 +33,8 @@ HIST_TOL = {"cholesky": 1e-8, "pcg": 1e-6}
 
 @pytest.mark.parametrize("inner", ["cholesky", "pcg"])
 @pytest.mark.parametrize("name", ["mgrit_cfg1", "mgrit_cfg2_delayed_n32",
-                                  "mgrit_cfg2_direct_n32"])
+                                  "mgrit_cfg2_direct_n32", "mgrit_cfg2_fcycle_n32",
+                                  "mgrit_cfg2_nested_n32"])
 def test_mgrit_matches_reference_engine(cuda, name, inner):
     """Same iteration count and residual history as the reference's own
     engine (mgrit.py) on the same model; C-point iterate within 1e-9."""

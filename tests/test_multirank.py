@@ -93,3 +93,28 @@ def test_engine_matches_oracle_engine():
     np.testing.assert_allclose([run1.initial_residual] + run1.residual_norms,
                                [ro.initial_residual] + ro.residual_norms, rtol=1e-10)
     np.testing.assert_allclose(sol1.numpy(), so, rtol=0, atol=1e-12 * np.abs(so).max())
+
+
+@pytest.mark.parametrize("kind,nested", [("F", False), ("V", True)])
+def test_cycle_variants_match_oracle_engine(kind, nested):
+    """F-cycle (mgrit.py:617-626) and nested iterations (mgrit.py:659-675)."""
+    from cpu_double import CpuDoubleProblem
+    from oracle import fem2d, mgrit as om, time_hierarchy as oth
+    from paper_1912_03106_b200 import (CycleSpec, MgritSolver, NullTransport,
+                                       StoppingCriterion, TimeHierarchy, build_uniform_grid)
+    spec = configs.config2(N=16, n_steps=512, levels=3, grids=2, strategy="delayed")
+    grid = build_uniform_grid(0.0, spec["tf"], spec["n_steps"])
+    solver = MgritSolver(CpuDoubleProblem(spec), TimeHierarchy.build(grid, [16, 16]),
+                         CycleSpec(kind=kind, gamma=1, max_iters=4, spatial_strategy="delayed",
+                                   nested_iterations=nested),
+                         StoppingCriterion(tolerance=1e-7), NullTransport())
+    run, sol = solver.solve()
+    g = oth.build_uniform_grid(0.0, spec["tf"], spec["n_steps"])
+    ro, so = om.mgrit_solve(fem2d.make_problem(spec), oth.TimeHierarchy.build(g, [16, 16]),
+                            om.CycleSpec(kind=kind, gamma=1, max_iters=4,
+                                         spatial_strategy="delayed", nested_iterations=nested),
+                            om.StoppingCriterion(tolerance=1e-7))
+    assert run.iterations == ro.iterations
+    np.testing.assert_allclose([run.initial_residual] + run.residual_norms,
+                               [ro.initial_residual] + ro.residual_norms, rtol=1e-10)
+    np.testing.assert_allclose(sol.numpy(), so, rtol=0, atol=1e-12 * np.abs(so).max())

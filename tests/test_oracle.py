@@ -24,12 +24,14 @@ def _oracle_run(fx):
     return om.mgrit_solve(prob, hier,
                           om.CycleSpec(kind=mg["kind"], gamma=mg["gamma"],
                                        max_iters=int(fx["max_iters"]),
-                                       spatial_strategy=mg["spatial_strategy"]),
+                                       spatial_strategy=mg["spatial_strategy"],
+                                       nested_iterations=mg.get("nested_iterations", False)),
                           om.StoppingCriterion(tolerance=float(fx["tol"])))
 
 
 @pytest.mark.parametrize("name", ["mgrit_cfg1", "mgrit_cfg2_delayed_n32",
-                                  "mgrit_cfg2_direct_n32"])
+                                  "mgrit_cfg2_direct_n32", "mgrit_cfg2_fcycle_n32",
+                                  "mgrit_cfg2_nested_n32"])
 def test_oracle_engine_reproduces_reference_engine(name):
     fx = load_golden(name)
     run, sol = _oracle_run(fx)
