@@ -441,15 +441,16 @@ static int ensure_ws(pg_ctx* ctx, Level& L, int B) {
     CU(cudaMemset(W.gcnt, 0, 8));
     if (L.n_elem > 0) {
         NewtonWork& N = L.NW;
-        if ((rc = alloc((void**)&N.u, vec)) || (rc = alloc((void**)&N.delta, vec)) ||
-            (rc = alloc((void**)&N.rhs, vec)) || (rc = alloc((void**)&N.res, vec)) ||
-            (rc = alloc((void**)&N.ucur, vec)) || (rc = alloc((void**)&N.dinv, vec)) ||
-            (rc = alloc((void**)&N.scale, B * 8)) || (rc = alloc((void**)&N.rnorm, B * 8)) ||
-            (rc = alloc((void**)&N.tnorm, B * 8)) || (rc = alloc((void**)&N.alpha, B * 8)) ||
-            (rc = alloc((void**)&N.state, B * 4)) || (rc = alloc((void**)&N.nit, B * 4)) ||
-            (rc = alloc((void**)&N.halv, B * 4)) || (rc = alloc((void**)&N.zero, B * 8)))
+        const size_t ev = (size_t)B * L.n_elem * 4 * sizeof(double);
+        if ((rc = alloc((void**)&N.u, vec)) || (rc = alloc((void**)&N.F, vec)) ||
+            (rc = alloc((void**)&N.d, vec)) || (rc = alloc((void**)&N.rhs, vec)) ||
+            (rc = alloc((void**)&N.tr, vec)) || (rc = alloc((void**)&N.pr, vec)) ||
+            (rc = alloc((void**)&N.pp, vec)) || (rc = alloc((void**)&N.pq, vec)) ||
+            (rc = alloc((void**)&N.dinv, vec)) || (rc = alloc((void**)&N.E, ev)) ||
+            (rc = alloc((void**)&N.Et, ev)) || (rc = alloc((void**)&N.nit, B * 4)) ||
+            (rc = alloc((void**)&N.status, B * 4)) || (rc = alloc((void**)&N.n_failed, 8)) ||
+            (rc = alloc((void**)&N.newton, 8)))
             return rc;
-        CU(cudaMemset(N.zero, 0, B * 8));
     }
     L.ws_B = B;
     return PG_OK;
@@ -936,6 +937,10 @@ extern "C" int pg_phi_batch(pg_ctx* ctx, int level, int B, const double* u_prev,
     if (L.n_elem > 0) {
         rc = newton_batch(ctx, L, B, u_prev, guess, inv_dt, src, u_out, st);
         if (rc) return rc;
+        dim3 grid(std::max(1, std::min(64, (L.n + 255) / 256)), B);
+        k_newton_out<<<grid, 256, 0, st>>>(L.n, B, L.NW.u, u_out, g, g_idx);
+        LAUNCHED();
+        return PG_OK;
     } else if (ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok) {
         return band_phi(ctx, L, B, u_prev, inv_dt, src, u_out, g, g_idx, st);
     } else if (L.resident) {

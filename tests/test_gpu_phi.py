@@ -50,6 +50,22 @@ def test_phi_batch_matches_oracle(cuda, name, smooth, inner):
         assert err.max() < TOL[inner], (name, g, err.max(), st)
 
 
+@pytest.mark.parametrize("smooth", [False, True])
+def test_nonlinear_newton_phi_matches_oracle(cuda, smooth):
+    """Batched damped Newton (problems.py:201-244) with matrix-free element
+    Jacobian + Jacobi-PCG vs the oracle's banded-Jacobian Newton; both stop
+    at |F| <= 1e-8 |rhs| along the same trajectory."""
+    fx = load_golden("phi_cfg3_n32")
+    prob = _problem(fx["spec"])
+    assert prob.nonlinear
+    for g in range(prob.spatial.n_grids):
+        ref = fx[f"phis{g}" if smooth else f"phi{g}"]
+        got, st = _phi(prob, g, fx[f"u{g}"], fx[f"tp{g}"], fx[f"tn{g}"], smooth)
+        err = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
+        assert err.max() < 1e-8, (g, err.max(), st)
+        assert st["newton_iters"] > 0
+
+
 def test_cholesky_many_dt_and_rhs_add(cuda):
     """Columns with 5 distinct dt (5 factors, grouped/permuted columns) and
     the fused g add, vs the oracle."""
