@@ -16,9 +16,14 @@ value  : whole-job fine time-step*DOF/s = n_steps * n_dofs * K / t, inputs
          barrier + synchronize on both sides, max over ranks.
 e2e    : the same metric through the public API from host data: problem
          construction (host assembly, H2D of the level data and excitation
-         tables) + mgrit_solve(gather_solution=True) + D2H of the trajectory.
-roofline: the dominant kernel of the solve (streamed Jacobi-PCG), algorithmic
-         bytes per launch / CUDA-event launch duration, vs MEASURED_PEAKS.json.
+         tables), factorisation, solve, D2H of the C-point solution (the MGRIT
+         iterate, 132 MB) into pinned host memory.
+sequential_gpu_s: the same problem by plain sequential stepping on the GPU
+         (2^14 dependent Phi calls) -- what time parallelism is measured against.
+roofline: the dominant kernel of the solve (k_band_solve: fp64 DMMA; the
+         Jacobi-PCG kernels in phi_microbench), algorithmic work per launch /
+         CUDA-event launch duration, vs MEASURED_PEAKS.json (HBM) or the
+         nominal fp64 peak.
 cpu_baseline: the CPU oracle port (oracle/, reference algorithm restated:
          reference MGRIT engine order + banded Cholesky Phi) on a bounded
          window of the same workload, one core.
@@ -341,7 +346,11 @@ def run_b200(args):
         elapsed = float(t.item())
     value = args.steps * n_steps * n0 / elapsed
 
-    # --- end to end through the public API, host data in, host trajectory out
+    # --- end to end through the public API: host spec in (assembly + H2D of
+    # the level data and excitation tables, factorisation), solve, D2H of the
+    # solution at the C-points (the MGRIT iterate) into pinned host memory
+    lvl0 = solver.levels[0]
+    host = torch.empty((lvl0.K, lvl0.n), dtype=torch.float64, pin_memory=True)
     barrier()
     t0 = time.perf_counter()
     p2 = GpuFemProblem(spec, device=local)
@@ -350,17 +359,31 @@ def run_b200(args):
     s2, _ = make_solver(p2)
     h2d += sum(lv.inv_dt_all.numel() * 8 + sum(t.numel() * 8 for t in lv.src_all)
                for lv in s2.levels)
-    run2, sol = s2.solve(gather_solution=True)
-    host = sol.cpu().numpy() if sol is not None else None
+    run2, _ = s2.solve(gather_solution=False)
+    host.copy_(s2.levels[0].c_store, non_blocking=True)
     barrier()
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    d2h = int(host.nbytes) if host is not None else 0
-    del host, sol
+    d2h = int(host.numel() * 8)
+    del host
     p2.close()
+
+    # --- GPU sequential time stepping (the time-to-solution baseline)
+    seq_s = None
+    if world == 1 and not args.no_seq:
+        from paper_1912_03106_b200 import sequential_solve
+        grid = build_uniform_grid(0.0, spec["tf"], n_steps)
+        traj = sequential_solve(problem, grid.points[:65])        # warm (factors)
+        barrier()
+        e0.record(stream)
+        traj = sequential_solve(problem, grid.points)
+        e1.record(stream)
+        barrier()
+        seq_s = e0.elapsed_time(e1) / 1e3
+        del traj
 
     if rank != 0:
         return 0
@@ -403,6 +426,8 @@ def run_b200(args):
         "data": "synthetic (BASELINE config 2 model, no external data)",
         "config": workload_config(spec, world),
         "time_to_solution_s": elapsed / args.steps,
+        "sequential_gpu_s": seq_s,
+        "speedup_vs_sequential_gpu": (seq_s / (elapsed / args.steps)) if seq_s else None,
         "mgrit": {"iterations": r.iterations, "converged": r.converged,
                   "residual_history": [r.initial_residual] + list(r.residual_norms),
                   "phi_columns_per_solve": r.phi_columns, "phi_calls_per_solve": r.phi_calls},
@@ -428,6 +453,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-phi", action="store_true", help="skip the config-5 batched-Phi leg")
+    ap.add_argument("--no-seq", action="store_true", help="skip the GPU sequential-stepping leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -78,11 +78,12 @@ class Excitation:
         return self._ramp(t) * self.modulation * reference(phase, t, self.period)
 
     def table(self, phases, times, smooth=False):
-        """[len(times), len(phases)] values (scalar-evaluated, like the
-        reference's per-call forcing)."""
+        """[len(times), len(phases)] values, the same formulas evaluated on the
+        whole time array at once (tests/test_host.py checks them against the
+        scalar oracle bit for bit)."""
         f = self.smooth_value if smooth else self.value
+        times = np.asarray(times, dtype=float)
         out = np.zeros((len(times), len(phases)))
         for k, ph in enumerate(phases):
-            for i, t in enumerate(times):
-                out[i, k] = float(f(ph, float(t)))
+            out[:, k] = np.broadcast_to(f(ph, times), times.shape)
         return out
