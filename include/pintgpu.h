@@ -124,6 +124,15 @@ int  pg_phi_batch(pg_ctx* ctx, int level, int B,
                   double* u_out, const double* g, const int32_t* g_idx,
                   void* stream);
 
+/* Same, with an optional HOST copy of inv_dt (identical values): the banded-
+ * Cholesky path then needs no device->host read to pick its per-dt factors,
+ * and caches the column grouping per distinct inv_dt pattern. */
+int  pg_phi_batch_h(pg_ctx* ctx, int level, int B,
+                    const double* u_prev, const double* guess,
+                    const double* inv_dt, const double* inv_dt_host, const double* src,
+                    double* u_out, const double* g, const int32_t* g_idx,
+                    void* stream);
+
 /* Statistics of the most recent pg_phi_batch (synchronises the stream). */
 int  pg_last_stats(pg_ctx* ctx, pg_phi_stats* out);
 /* Cumulative statistics since the context was created / reset. */

@@ -10,22 +10,22 @@
 //        FL[k] = [ D_k^-1 | L(k rows, W cols before k) ]      (forward)
 //        FU[k] = [ D_k^-T | L(W rows after k, k cols)^T ]     (backward)
 //    each nb x LDA row-major (LDA = nb + W + 4: bank-conflict padding).
-//  * k_band_solve<FWD/BWD>: each CTA walks all block rows for a chunk of BC
-//    columns sharing one factor.  Per block row: TMA bulk-copies the next
-//    block's operands (2-stage mbarrier ring) while the current block does
-//        acc = rhs_blk - Lwin * y_window      (nb x W x BC)
-//        y_blk = D^-1 acc                     (nb x nb x BC)
-//    as fp64 tensor-core MMAs (mma.sync m8n8k4 f64: SASS DMMA), the window
-//    living in a shared-memory ring of the last W/nb blocks.
+//  * forward  L y = b:  y_k = D_k^-1 b_k - (D_k^-1 L_win,k) y_window
+//    backward L^T x = y: x_k = D_k^-T y_k - (D_k^-T U_win,k) x_window
+//    k_band_chain walks the block rows for a chunk of BC columns sharing one
+//    factor: per block step two independent fp64 tensor-core GEMM chains
+//    (mma.sync m8n8k4, SASS DMMA) -- D^-1 b_k on b staged one step ahead, and
+//    the window product -- and one barrier; the next block's operands are
+//    TMA-prefetched (2-stage mbarrier ring), the window is a smem ring.
 //
-// Explicit inverses of the 32 x 32 diagonal blocks turn the triangular
-// solves into GEMMs; the factor is otherwise the same arithmetic as dpbtrf.
+// Folding the explicit 32 x 32 diagonal-block inverses into the window
+// operators at factor time leaves one GEMM on the sequential critical path;
+// the factorisation itself is the same arithmetic as dpbtrf.
 #pragma once
 #include "common.cuh"
 #include "tma.cuh"
 
 #define BD_NB 32
-#define BD_NT 256          // 8 warps: 4 row groups x 2 window halves
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
     asm volatile(
@@ -38,7 +38,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // factorisation: one CTA per factor, 256 threads
 // LB[i][d] = A[i][i-d] (d = 0..w), A = c M + K built from the CSR (lower part)
 struct BandFactorArgs {
-    int n, w, W, LDA, nblk;
+    int n, w, W, LDA, nblk;     // LDA: row stride of the chain operands (W + 4)
     const int* row_ptr;
     const int* col_idx;
     const double* m_val;
@@ -61,7 +61,11 @@ k_band_build(BandFactorArgs a, const double* __restrict__ cvals, double* const* 
     }
 }
 
-// smem: D[32][33], Dinv[32][33], P[w][33]
+// smem: D[32][33], Dinv[32][33], P[w][33], Lw[32][W]
+// Per block row k it emits FL[k] = [D_k^-1 | D_k^-1 L_win] and
+// FU[k] = [D_k^-T | D_k^-T U_win] (32 x LDA, LDA = 32 + W + 4): the solve
+// step is y_k = D_k^-1 b_k - (D_k^-1 L_win) y_win, whose first term does not
+// depend on the chain.
 __global__ void __launch_bounds__(256)
 k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* const* FUs,
               int* status) {
@@ -74,6 +78,7 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
     double* D = sm;
     double* Di = D + NB * S;
     double* P = Di + NB * S;
+    double* Lw = P + (size_t)a.w * S;
     const int stride = a.w + 1;
     const int tid = threadIdx.x;
     auto lb = [&](int i, int j) -> double& { return LB[(size_t)i * stride + (i - j)]; };
@@ -152,21 +157,31 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
             if (j < kb && gr - gc <= a.w) lb(gr, gc) = P[r * S + j];
         }
         // 5. solve operands of block k
+        //    Lw[i][q] = L[k0+i][k0-W+q] (final: earlier panels)
+        for (int t = tid; t < NB * a.W; t += blockDim.x) {
+            const int i = t / a.W, q = t % a.W;
+            const int gr = k0 + i, gc = k0 - a.W + q;
+            Lw[t] = (i < kb && gc >= 0 && gr - gc <= a.w) ? lb(gr, gc) : 0.0;
+        }
+        __syncthreads();
         double* fl = FL + (size_t)k * NB * a.LDA;
         double* fu = FU + (size_t)k * NB * a.LDA;
         for (int t = tid; t < NB * a.LDA; t += blockDim.x) {
             const int i = t / a.LDA, j = t % a.LDA;
             double vl = 0.0, vu = 0.0;
             if (j < NB) {
-                vl = Di[i * S + j];              // D^-1
-                vu = Di[j * S + i];              // D^-T
+                vl = Di[i * S + j];                 // D^-1
+                vu = Di[j * S + i];                 // D^-T
             } else if (j < NB + a.W) {
-                const int q = j - NB;            // window column
-                // forward: L[k0+i][k0-W+q]  (final: earlier panels)
-                const int gr = k0 + i, gc = k0 - a.W + q;
-                if (i < kb && gc >= 0 && gr - gc <= a.w) vl = lb(gr, gc);
-                // backward: L[k0+NB+q][k0+i] = P[q][i]
-                if (q < m && i < kb && (r0 + q) - (k0 + i) <= a.w) vu = P[q * S + i];
+                const int q = j - NB;
+                // (D^-1 L_win)[i][q] = sum_p Di[i][p] Lw[p][q]
+#pragma unroll 8
+                for (int p = 0; p <= i; ++p) vl = fma(Di[i * S + p], Lw[p * a.W + q], vl);
+                // (D^-T U_win)[i][q] = sum_p Di[p][i] P[q][p]
+                if (q < m) {
+#pragma unroll 8
+                    for (int p = i; p < NB; ++p) vu = fma(Di[p * S + i], P[q * S + p], vu);
+                }
             }
             fl[t] = vl;
             fu[t] = vu;
@@ -187,150 +202,232 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
 
 // ---------------------------------------------------------------------------
 // batched solves
+#define BD_MAXST 2
+constexpr int NST = 2;           // TMA ring depth (see band_stages)
 struct BandSolveArgs {
     int np, W, LDA, nblk, ldy;
+    int nst;                     // TMA ring depth (2..BD_MAXST)
     double* Y;                   // [n_cols][ldy] grouped columns, in place
     const int4* chunks;          // (factor, first grouped column, count, 0)
-    double* const* F;            // per factor: FL or FU base
+    double* const* F;            // per factor: FL or FU base (chain operands)
 };
 
-// smem layout (doubles): stage[2][NB * LDA], ring[NSLOT][NB][BC + 4], T[NB][BC + 4]
-// 8 warps: warp w -> row group rg = w & 3 (rows 8 rg .. 8 rg + 7) and window
-// half kh = w >> 2.  The window (NSLOT = W / 32 blocks, a power of two, so
-// ring slots are masks) is fully unrolled; each warp keeps four independent
-// DMMA accumulator chains; the two halves are summed through T.
+// The sequential chain:  y_k = D_k^-1 b_k - (D_k^-1 L_win) y_window.
+// 4 warps, warp w owns rows 8w..8w+7.  Per block step: one DMMA chain for
+// D_k^-1 b_k (b_k staged in smem one step ahead -- independent of the
+// window) plus NCH chains over the window, a single barrier.  The next
+// block's operands arrive by TMA (2-stage mbarrier ring); the window is a
+// shared-memory ring holding the last 2*NSLOT blocks.
+// smem (doubles): stage[2][NB * LDA], ring[2 NSLOT][NB][BC + 4], sb[2][NB][BC + 4]
+#define BD_CT 128
 template <int BC, int NSLOT, bool FWD>
-__global__ void __launch_bounds__(BD_NT)
-k_band_solve(BandSolveArgs a) {
+__global__ void __launch_bounds__(BD_CT)
+k_band_chain(BandSolveArgs a) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(8) uint64_t bar[BD_MAXST];
     const int4 ch = a.chunks[blockIdx.x];
     const double* F = a.F[ch.x];
     const int col0 = ch.y, ncol = ch.z;
     constexpr int NB = BD_NB, RS = BC + 4, NT8 = BC / 8;
     constexpr int W = NSLOT * NB;
-    // per-half window rows: [kh * HALF, kh * HALF + HALF)
-    constexpr int HALF = W / 2;
+    constexpr int NCH = W >= 128 ? 8 : 4;
+    constexpr int RMASK = 2 * NSLOT - 1;
     double* stage = sm;
-    double* ring = stage + 2 * (size_t)NB * a.LDA;
-    double* T = ring + (size_t)NSLOT * NB * RS;
+    double* ring = stage + (size_t)NST * NB * a.LDA;
+    double* sb = ring + (size_t)2 * NSLOT * NB * RS;   // [2][NB][RS]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q4 = lane & 3;
-    const int rg = warp & 3, kh = warp >> 2;
-    const int lrow = 8 * rg + g;
+    const int lrow = 8 * warp + g;
     const uint32_t blk_bytes = (uint32_t)(NB * a.LDA * 8);
+    // b staging: thread t moves (row t & 31, columns (t >> 5) + 4 j)
+    constexpr int BPT = BC / 4;
+    const int brow = threadIdx.x & 31, bcol = threadIdx.x >> 5;
 
-    for (int t = threadIdx.x; t < NSLOT * NB * RS; t += BD_NT) ring[t] = 0.0;
+    for (int t = threadIdx.x; t < 2 * NSLOT * NB * RS; t += BD_CT) ring[t] = 0.0;
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
         mbar_fence_init();
     }
-    __syncthreads();
     auto blk_of = [&](int s) { return FWD ? s : a.nblk - 1 - s; };
+    double breg[BPT];
+    auto load_b = [&](int s) {
+        const int rr = NB * blk_of(s) + brow;
+#pragma unroll
+        for (int j = 0; j < BPT; ++j) {
+            const int cc = bcol + 4 * j;
+            breg[j] = cc < ncol ? a.Y[(size_t)(col0 + cc) * a.ldy + rr] : 0.0;
+        }
+    };
+    auto store_b = [&](int buf) {
+#pragma unroll
+        for (int j = 0; j < BPT; ++j) sb[((size_t)buf * NB + brow) * RS + bcol + 4 * j] = breg[j];
+    };
+    load_b(0);
+    store_b(0);
+    if (a.nblk > 1) load_b(1);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(&bar[0], blk_bytes);
-        tma_load_1d(stage, F + (size_t)blk_of(0) * NB * a.LDA, blk_bytes, &bar[0]);
+        for (int q = 0; q + 1 < NST && q < a.nblk; ++q) {
+            mbar_arrive_expect_tx(&bar[q], blk_bytes);
+            tma_load_1d(stage + (size_t)q * NB * a.LDA, F + (size_t)blk_of(q) * NB * a.LDA,
+                        blk_bytes, &bar[q]);
+        }
     }
-    double nxt[NT8][2];
-    auto load_rhs = [&](int s) {
-        const int rrow = NB * blk_of(s) + lrow;
+    for (int s = 0; s < a.nblk; ++s) {
+        const int k = blk_of(s);
+        const int st = s & 1;
+        const int sb_cur = s & 1;
+        // keep nst - 1 blocks in flight: issue block s + nst - 1 into the stage
+        // freed by block s - 1 (all threads passed the previous barrier)
+        if (threadIdx.x == 0 && s + NST - 1 < a.nblk) {
+            const int sn = (s + 1) & 1;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bar[sn], blk_bytes);
+            tma_load_1d(stage + (size_t)sn * NB * a.LDA,
+                        F + (size_t)blk_of(s + NST - 1) * NB * a.LDA, blk_bytes, &bar[sn]);
+        }
+        // b of block s+1 (in registers since the previous step) -> smem; prefetch s+2
+        if (s + 1 < a.nblk) {
+            store_b(sb_cur ^ 1);
+            if (s + 2 < a.nblk) load_b(s + 2);
+        }
+        double acc[NCH][NT8][2], dacc[2][NT8][2];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt) dacc[c][nt][0] = dacc[c][nt][1] = 0.0;
+        const int row = NB * k + lrow;
+        mbar_wait(&bar[st], (s >> 1) & 1);
+        const double* Lrow = stage + (size_t)st * NB * a.LDA + lrow * a.LDA;
+        // D_k^-1 b_k  (independent of the window)
+        const double* bb = sb + (size_t)sb_cur * NB * RS;
+#pragma unroll
+        for (int j = 0; j < NB; j += 4) {
+            const double av = Lrow[j + q4];
+            const double* rr = bb + (j + q4) * RS + g;
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt)
+                dmma_8x8x4(dacc[(j >> 2) & 1][nt][0], dacc[(j >> 2) & 1][nt][1], av, rr[8 * nt]);
+        }
+        // - (D_k^-1 L_win) y_window
+#pragma unroll
+        for (int j = 0; j < W; j += 4) {
+            const int wbi = j / NB;
+            const int blk = FWD ? (k - NSLOT + wbi) : (k + 1 + wbi);
+            const bool ok = FWD ? (blk >= 0) : (blk < a.nblk);
+            const int slot = blk & RMASK;
+            const double av = -Lrow[NB + j + q4];
+            const double* rr = ring + ((size_t)slot * NB + (j % NB) + q4) * RS + g;
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt) {
+                const double bv = ok ? rr[8 * nt] : 0.0;
+                dmma_8x8x4(acc[(j >> 2) % NCH][nt][0], acc[(j >> 2) % NCH][nt][1], av, bv);
+            }
+        }
+        double* slotp = ring + (size_t)(k & RMASK) * NB * RS;
 #pragma unroll
         for (int nt = 0; nt < NT8; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int cc = 8 * nt + 2 * q4 + h;
-                nxt[nt][h] = (kh == 0 && cc < ncol) ? a.Y[(size_t)(col0 + cc) * a.ldy + rrow] : 0.0;
+                double v = dacc[0][nt][h] + dacc[1][nt][h];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) v += acc[c][nt][h];
+                slotp[lrow * RS + cc] = v;
+                if (cc < ncol) a.Y[(size_t)(col0 + cc) * a.ldy + row] = v;
             }
-    };
-    load_rhs(0);
+        __syncthreads();            // block k visible in the ring; stage / sb buffers free
+    }
+}
+
+// One-column chain for small batches (B <= #SMs: the coarsest chain, the
+// sequential stepper, sparse coarse levels): 128 threads = 32 rows x 4 lanes,
+// each lane a quarter of the K = 32 + W dot product with plain fp64 FMAs in
+// two accumulators, reduced by two shuffles; one barrier per block step.
+// smem (doubles): stage[2][NB * LDA], ring[2 NSLOT][NB], sb[2][NB]
+template <int NSLOT, bool FWD>
+__global__ void __launch_bounds__(BD_CT)
+k_band_chain1(BandSolveArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t bar[BD_MAXST];
+    const int4 ch = a.chunks[blockIdx.x];
+    const double* F = a.F[ch.x];
+    const int col = ch.y;
+    constexpr int NB = BD_NB;
+    constexpr int W = NSLOT * NB;
+    constexpr int RMASK = 2 * NSLOT - 1;
+    double* stage = sm;
+    double* ring = stage + (size_t)NST * NB * a.LDA;
+    double* sb = ring + 2 * NSLOT * NB;
+    const int r = threadIdx.x >> 2, sub = threadIdx.x & 3;
+    const uint32_t blk_bytes = (uint32_t)(NB * a.LDA * 8);
+    double* Ycol = a.Y + (size_t)col * a.ldy;
+
+    for (int t = threadIdx.x; t < 2 * NSLOT * NB; t += BD_CT) ring[t] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
+        mbar_fence_init();
+    }
+    auto blk_of = [&](int s) { return FWD ? s : a.nblk - 1 - s; };
+    double breg = 0.0;
+    if (threadIdx.x < NB) sb[threadIdx.x] = Ycol[NB * blk_of(0) + threadIdx.x];
+    if (threadIdx.x < NB && a.nblk > 1) breg = Ycol[NB * blk_of(1) + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 0; q + 1 < NST && q < a.nblk; ++q) {
+            mbar_arrive_expect_tx(&bar[q], blk_bytes);
+            tma_load_1d(stage + (size_t)q * NB * a.LDA, F + (size_t)blk_of(q) * NB * a.LDA,
+                        blk_bytes, &bar[q]);
+        }
+    }
     for (int s = 0; s < a.nblk; ++s) {
         const int k = blk_of(s);
         const int st = s & 1;
-        if (threadIdx.x == 0 && s + 1 < a.nblk) {
+        const int sb_cur = s & 1;
+        // keep nst - 1 blocks in flight: issue block s + nst - 1 into the stage
+        // freed by block s - 1 (all threads passed the previous barrier)
+        if (threadIdx.x == 0 && s + NST - 1 < a.nblk) {
+            const int sn = (s + 1) & 1;
             fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&bar[st ^ 1], blk_bytes);
-            tma_load_1d(stage + (size_t)(st ^ 1) * NB * a.LDA,
-                        F + (size_t)blk_of(s + 1) * NB * a.LDA, blk_bytes, &bar[st ^ 1]);
+            mbar_arrive_expect_tx(&bar[sn], blk_bytes);
+            tma_load_1d(stage + (size_t)sn * NB * a.LDA,
+                        F + (size_t)blk_of(s + NST - 1) * NB * a.LDA, blk_bytes, &bar[sn]);
         }
-        double acc[4][NT8][2];
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int nt = 0; nt < NT8; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
-#pragma unroll
-        for (int nt = 0; nt < NT8; ++nt) {
-            acc[0][nt][0] = nxt[nt][0];
-            acc[0][nt][1] = nxt[nt][1];
+        if (threadIdx.x < NB && s + 1 < a.nblk) {
+            sb[(sb_cur ^ 1) * NB + threadIdx.x] = breg;
+            if (s + 2 < a.nblk) breg = Ycol[NB * blk_of(s + 2) + threadIdx.x];
         }
-        const int row = NB * k + lrow;
-        if (s + 1 < a.nblk) load_rhs(s + 1);
         mbar_wait(&bar[st], (s >> 1) & 1);
-        const double* Lt = stage + (size_t)st * NB * a.LDA;
-        const double* Lrow = Lt + lrow * a.LDA + NB;
-        // window: rows j in [kh*HALF, kh*HALF + HALF); block wbi = j / NB
-        const int kbeg = kh * HALF;
+        const double* Lrow = stage + (size_t)st * NB * a.LDA + r * a.LDA;
+        const double* bb = sb + sb_cur * NB;
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-        for (int jj = 0; jj < HALF; jj += 4) {
-            const int j = kbeg + jj;                    // uniform per warp
-            const int wbi = j / NB;                     // j multiple of 4: exact
-            const int blk = FWD ? (k - NSLOT + wbi) : (k + 1 + wbi);
-            const bool ok = FWD ? (blk >= 0) : (blk < a.nblk);
-            const int slot = (FWD ? (k + wbi) : (k + 1 + wbi)) & (NSLOT - 1);
-            const double av = -Lrow[j + q4];
-            const double* rr = ring + ((size_t)slot * NB + (j % NB) + q4) * RS + g;
-#pragma unroll
-            for (int nt = 0; nt < NT8; ++nt) {
-                const double bv = ok ? rr[8 * nt] : 0.0;
-                dmma_8x8x4(acc[(jj >> 2) & 3][nt][0], acc[(jj >> 2) & 3][nt][1], av, bv);
-            }
+        for (int j = sub; j < NB; j += 8) {
+            a0 = fma(Lrow[j], bb[j], a0);
+            a1 = fma(Lrow[j + 4], bb[j + 4], a1);
         }
-        double r0v[NT8][2];
 #pragma unroll
-        for (int nt = 0; nt < NT8; ++nt)
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-                r0v[nt][h] = (acc[0][nt][h] + acc[1][nt][h]) + (acc[2][nt][h] + acc[3][nt][h]);
-        if (kh == 1) {
-#pragma unroll
-            for (int nt = 0; nt < NT8; ++nt) {
-                T[lrow * RS + 8 * nt + 2 * q4] = r0v[nt][0];
-                T[lrow * RS + 8 * nt + 2 * q4 + 1] = r0v[nt][1];
-            }
+        for (int j = sub; j < W; j += 8) {
+            const int jb0 = j / NB, jb1 = (j + 4) / NB;
+            const int b0 = FWD ? (k - NSLOT + jb0) : (k + 1 + jb0);
+            const int b1 = FWD ? (k - NSLOT + jb1) : (k + 1 + jb1);
+            const bool ok0 = FWD ? (b0 >= 0) : (b0 < a.nblk);
+            const bool ok1 = FWD ? (b1 >= 0) : (b1 < a.nblk);
+            const double w0 = ok0 ? ring[(b0 & RMASK) * NB + (j % NB)] : 0.0;
+            const double w1 = ok1 ? ring[(b1 & RMASK) * NB + ((j + 4) % NB)] : 0.0;
+            a0 = fma(-Lrow[NB + j], w0, a0);
+            a1 = fma(-Lrow[NB + j + 4], w1, a1);
         }
-        __syncthreads();
-        if (kh == 0) {
-#pragma unroll
-            for (int nt = 0; nt < NT8; ++nt) {
-                T[lrow * RS + 8 * nt + 2 * q4] += r0v[nt][0];
-                T[lrow * RS + 8 * nt + 2 * q4 + 1] += r0v[nt][1];
-            }
-        }
-        __syncthreads();
-        if (kh == 0) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-#pragma unroll
-                for (int nt = 0; nt < NT8; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
-            const double* Ld = Lt + lrow * a.LDA;
-#pragma unroll
-            for (int kq = 0; kq < NB; kq += 4) {
-                const double av = Ld[kq + q4];
-                const double* tt = T + (kq + q4) * RS + g;
-#pragma unroll
-                for (int nt = 0; nt < NT8; ++nt)
-                    dmma_8x8x4(acc[(kq >> 2) & 3][nt][0], acc[(kq >> 2) & 3][nt][1], av, tt[8 * nt]);
-            }
-            double* slot = ring + (size_t)(k & (NSLOT - 1)) * NB * RS;
-#pragma unroll
-            for (int nt = 0; nt < NT8; ++nt)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int cc = 8 * nt + 2 * q4 + h;
-                    const double v = (acc[0][nt][h] + acc[1][nt][h]) + (acc[2][nt][h] + acc[3][nt][h]);
-                    slot[lrow * RS + cc] = v;
-                    if (cc < ncol) a.Y[(size_t)(col0 + cc) * a.ldy + row] = v;
-                }
+        double v = a0 + a1;
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (sub == 0) {
+            ring[(k & RMASK) * NB + r] = v;
+            Ycol[NB * k + r] = v;
         }
         __syncthreads();
     }

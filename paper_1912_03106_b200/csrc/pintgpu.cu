@@ -55,6 +55,9 @@ struct Level {
     int* d_perm = nullptr;
     int4* d_chunks = nullptr;
     int perm_cap = 0;
+    // column grouping cache: hash of the inv_dt pattern -> device perm/chunks
+    struct Group { std::vector<double> key; int* perm; int4* chunks; int nch; int BC; };
+    std::unordered_map<uint64_t, std::vector<Group>> groups;
     int* d_status = nullptr;
     // nonlinear iron elements
     int n_elem = 0;
@@ -194,14 +197,17 @@ extern "C" int pg_create(pg_ctx** out, int device) {
 static void free_level(Level& L) {
     void* ptrs[] = {L.row_ptr, L.col_idx, L.m_val, L.k_val, L.dM, L.dK, L.shapes,
                     L.weights, L.tile_lo, L.tile_hi, L.elem_dof, L.elem_geo,
-                    L.ne_ptr, L.ne, L.mk, L.d_FL, L.d_FU, L.Y, L.d_perm, L.d_chunks,
-                    L.d_status};
+                    L.ne_ptr, L.ne, L.mk, L.d_FL, L.d_FU, L.Y, L.d_perm,
+                    L.d_chunks, L.d_status};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : L.ws_allocs) cudaFree(p);
     L.ws_allocs.clear();
     for (double* p : L.FL) cudaFree(p);
     for (double* p : L.FU) cudaFree(p);
+    for (auto& kv : L.groups)
+        for (auto& gr : kv.second) { cudaFree(gr.perm); cudaFree(gr.chunks); }
+    L.groups.clear();
 }
 
 extern "C" void pg_destroy(pg_ctx* ctx) {
@@ -727,12 +733,24 @@ static int newton_batch(pg_ctx* ctx, Level& L, int B, const double* u_prev,
 // over ~B/8 SMs; 16 when the batch is large enough to fill the GPU anyway.
 static int band_solve_bc(const Level& L, int B, int n_sm) {
     (void)L;
+    if (B <= n_sm) return 1;          // one column per CTA: FMA chain
     return B >= 16 * n_sm ? 16 : 8;
 }
 
-static size_t band_solve_smem(const Level& L, int BC) {
-    return (size_t)(2 * BD_NB * L.LDA + (L.bwin / BD_NB) * BD_NB * (BC + 4) + BD_NB * (BC + 4)) *
-           sizeof(double);
+static size_t band_solve_smem(const Level& L, int BC, int nst) {
+    if (BC == 1)
+        return (size_t)(nst * BD_NB * L.LDA + 2 * L.bwin + 2 * BD_NB) * sizeof(double);
+    return (size_t)(nst * BD_NB * L.LDA + 2 * (L.bwin / BD_NB) * BD_NB * (BC + 4) +
+                    2 * BD_NB * (BC + 4)) * sizeof(double);
+}
+
+// TMA ring depth.  Measured (round 1): 2 stages beat 3-4 -- the chain is
+// bound by shared-memory traffic of the 42 KB factor block per step, and
+// more blocks in flight only add smem write pressure.
+static int band_stages(const Level& L, int BC) {
+    (void)L;
+    (void)BC;
+    return 2;
 }
 
 static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
@@ -774,7 +792,8 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     dim3 gb(std::min(1024, (L.n + 255) / 256), nf);
     k_band_build<<<gb, 256, 0, st>>>(a, d_c, d_lb);
     LAUNCHED();
-    const size_t sm = (size_t)(2 * BD_NB * (BD_NB + 1) + L.bw * (BD_NB + 1)) * sizeof(double);
+    const size_t sm = (size_t)(2 * BD_NB * (BD_NB + 1) + L.bw * (BD_NB + 1) + BD_NB * L.bwin) *
+                      sizeof(double);
     CU(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_band_factor<<<nf, 256, sm, st>>>(a, d_lb, L.d_FL + first, L.d_FU + first, L.d_status);
     LAUNCHED();
@@ -789,72 +808,113 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     return PG_OK;
 }
 
-template <int BC, int NS>
-static int launch_band(pg_ctx* ctx, BandSolveArgs sa, double** d_FU, int nch, size_t sm,
-                       cudaStream_t st) {
-    CU(cudaFuncSetAttribute(k_band_solve<BC, NS, true>,
+template <int NS>
+static int launch_band1(pg_ctx* ctx, BandSolveArgs sa, double** d_FU, int nch, size_t sm,
+                        cudaStream_t st) {
+    CU(cudaFuncSetAttribute(k_band_chain1<NS, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CU(cudaFuncSetAttribute(k_band_solve<BC, NS, false>,
+    CU(cudaFuncSetAttribute(k_band_chain1<NS, false>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_band_solve<BC, NS, true><<<nch, BD_NT, sm, st>>>(sa);
+    k_band_chain1<NS, true><<<nch, BD_CT, sm, st>>>(sa);
     LAUNCHED();
     sa.F = d_FU;
-    k_band_solve<BC, NS, false><<<nch, BD_NT, sm, st>>>(sa);
+    k_band_chain1<NS, false><<<nch, BD_CT, sm, st>>>(sa);
     LAUNCHED();
     return PG_OK;
 }
 
+template <int BC, int NS>
+static int launch_band(pg_ctx* ctx, BandSolveArgs sa, double** d_FU, int nch, size_t sm,
+                       cudaStream_t st) {
+    CU(cudaFuncSetAttribute(k_band_chain<BC, NS, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CU(cudaFuncSetAttribute(k_band_chain<BC, NS, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_band_chain<BC, NS, true><<<nch, BD_CT, sm, st>>>(sa);     // L y = b
+    LAUNCHED();
+    sa.F = d_FU;
+    k_band_chain<BC, NS, false><<<nch, BD_CT, sm, st>>>(sa);    // L^T x = y
+    LAUNCHED();
+    return PG_OK;
+}
+
+static uint64_t hash_doubles(const double* v, int n) {
+    uint64_t h = 1469598103934665603ull ^ (uint64_t)n;
+    for (int i = 0; i < n; ++i) {
+        uint64_t x;
+        memcpy(&x, v + i, 8);
+        h = (h ^ x) * 1099511628211ull;
+        h ^= h >> 29;
+    }
+    return h;
+}
+
 static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* inv_dt,
-                    const double* src, double* u_out, const double* g, const int* g_idx,
-                    cudaStream_t st) {
+                    const double* inv_dt_host, const double* src, double* u_out,
+                    const double* g, const int* g_idx, cudaStream_t st) {
     std::vector<double> c(B);
-    CU(cudaMemcpyAsync(c.data(), inv_dt, B * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    // factor index per column (cached per bitwise value of 1/dt, like the
-    // reference's (grid, float(dt)) cache), new factors in one launch
-    std::vector<int> fid(B);
-    std::vector<double> fresh;
-    std::unordered_map<uint64_t, int> pending;
-    for (int b = 0; b < B; ++b) {
-        uint64_t key;
-        memcpy(&key, &c[b], 8);
-        auto it = L.fac_index.find(key);
-        if (it != L.fac_index.end()) { fid[b] = it->second; continue; }
-        auto jt = pending.find(key);
-        if (jt == pending.end()) {
-            const int id = (int)L.FL.size() + (int)fresh.size();
-            pending[key] = id;
-            fresh.push_back(c[b]);
-            fid[b] = id;
-        } else {
-            fid[b] = jt->second;
-        }
+    if (inv_dt_host) {
+        memcpy(c.data(), inv_dt_host, B * sizeof(double));
+    } else {
+        CU(cudaMemcpyAsync(c.data(), inv_dt, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
     }
-    int rc = band_factors(ctx, L, fresh, st);
-    if (rc) return rc;
-    for (auto& kv : pending) L.fac_index[kv.first] = kv.second;
-    // group columns by factor -> perm, chunks of BC
     const int BC = band_solve_bc(L, B, ctx->n_sm);
-    std::vector<int> perm(B);
-    for (int b = 0; b < B; ++b) perm[b] = b;
-    std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return fid[x] < fid[y]; });
-    std::vector<int4> chunks;
-    for (int i = 0; i < B;) {
-        int j = i;
-        while (j < B && fid[perm[j]] == fid[perm[i]] && j - i < BC) ++j;
-        chunks.push_back(make_int4(fid[perm[i]], i, j - i, 0));
-        i = j;
+    // cached grouping for this exact inv_dt pattern?
+    const uint64_t h = hash_doubles(c.data(), B);
+    Level::Group* grp = nullptr;
+    for (auto& gr : L.groups[h])
+        if ((int)gr.key.size() == B && gr.BC == BC &&
+            memcmp(gr.key.data(), c.data(), B * sizeof(double)) == 0)
+            grp = &gr;
+    int rc;
+    std::vector<int> fid;
+    if (!grp) {
+        // factor index per column (cached per bitwise value of 1/dt, like the
+        // reference's (grid, float(dt)) cache), new factors in one launch
+        fid.resize(B);
+        std::vector<double> fresh;
+        std::unordered_map<uint64_t, int> pending;
+        for (int b = 0; b < B; ++b) {
+            uint64_t key;
+            memcpy(&key, &c[b], 8);
+            auto it = L.fac_index.find(key);
+            if (it != L.fac_index.end()) { fid[b] = it->second; continue; }
+            auto jt = pending.find(key);
+            if (jt == pending.end()) {
+                const int id = (int)L.FL.size() + (int)fresh.size();
+                pending[key] = id;
+                fresh.push_back(c[b]);
+                fid[b] = id;
+            } else {
+                fid[b] = jt->second;
+            }
+        }
+        if ((rc = band_factors(ctx, L, fresh, st))) return rc;
+        for (auto& kv : pending) L.fac_index[kv.first] = kv.second;
+        // group columns by factor -> perm, chunks of BC
+        std::vector<int> perm(B);
+        for (int b = 0; b < B; ++b) perm[b] = b;
+        std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return fid[x] < fid[y]; });
+        std::vector<int4> chunks;
+        for (int i = 0; i < B;) {
+            int j = i;
+            while (j < B && fid[perm[j]] == fid[perm[i]] && j - i < BC) ++j;
+            chunks.push_back(make_int4(fid[perm[i]], i, j - i, 0));
+            i = j;
+        }
+        Level::Group gr{c, nullptr, nullptr, (int)chunks.size(), BC};
+        CU(cudaMalloc(&gr.perm, B * sizeof(int)));
+        CU(cudaMalloc(&gr.chunks, chunks.size() * sizeof(int4)));
+        CU(cudaMemcpy(gr.perm, perm.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(gr.chunks, chunks.data(), chunks.size() * sizeof(int4),
+                      cudaMemcpyHostToDevice));
+        L.groups[h].push_back(gr);
+        grp = &L.groups[h].back();
     }
-    if (B > L.perm_cap) {
-        if (L.d_perm) cudaFree(L.d_perm);
-        if (L.d_chunks) cudaFree(L.d_chunks);
-        L.perm_cap = std::max(B, 64);
-        CU(cudaMalloc(&L.d_perm, L.perm_cap * sizeof(int)));
-        CU(cudaMalloc(&L.d_chunks, L.perm_cap * sizeof(int4)));
-    }
-    CU(cudaMemcpyAsync(L.d_perm, perm.data(), B * sizeof(int), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(L.d_chunks, chunks.data(), chunks.size() * sizeof(int4),
-                       cudaMemcpyHostToDevice, st));
+    const int* d_perm = grp->perm;
+    const int4* d_chunks = grp->chunks;
+    const int nch = grp->nch;
     if (B > L.Y_B) {
         if (L.Y) cudaFree(L.Y);
         L.Y_B = B;
@@ -862,16 +922,18 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     }
     dim3 gr(std::max(1, std::min(32, (L.np + 255) / 256)), B);
     k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, L.row_ptr, L.col_idx, L.m_val, L.n_src, L.shapes,
-                                   u_prev, inv_dt, src, L.d_perm, L.Y);
+                                   u_prev, inv_dt, src, d_perm, L.Y);
     LAUNCHED();
-    BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, L.Y, L.d_chunks, L.d_FL};
-    const size_t sm = band_solve_smem(L, BC);
-    const int nch = (int)chunks.size();
+    BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL};
+    const int nst = band_stages(L, BC);
+    const size_t sm = band_solve_smem(L, BC, nst);
+    sa.nst = std::max(2, std::min(nst, L.nblk));
     if ((rc = prof_mark(ctx, 2, st))) return rc;
     switch (L.bwin / BD_NB) {
 #define PG_BAND_CASE(NS)                                                                  \
     case NS:                                                                              \
-        if (BC == 8) rc = launch_band<8, NS>(ctx, sa, L.d_FU, nch, sm, st);              \
+        if (BC == 1) rc = launch_band1<NS>(ctx, sa, L.d_FU, nch, sm, st);                \
+        else if (BC == 8) rc = launch_band<8, NS>(ctx, sa, L.d_FU, nch, sm, st);         \
         else rc = launch_band<16, NS>(ctx, sa, L.d_FU, nch, sm, st);                     \
         break;
         PG_BAND_CASE(1)
@@ -888,9 +950,11 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         // 2 * 2 * np * (W + nb) flops; HBM bytes = Y in/out twice + each
         // distinct factor pair read once
         std::vector<char> used(L.FL.size(), 0);
-        for (int b = 0; b < B; ++b) used[fid[b]] = 1;
+        std::vector<int4> hch(nch);
+        CU(cudaMemcpy(hch.data(), d_chunks, nch * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (const int4& q : hch) used[q.x] = 1;
         double fb = 0.0;
-        for (char u : used) fb += u ? 2.0 * L.nblk * BD_NB * L.LDA * 8.0 : 0.0;
+        for (char u : used) fb += u ? 2.0 * L.LDA * L.nblk * BD_NB * 8.0 : 0.0;
         ctx->prof_flops[2] += 4.0 * L.np * (double)(L.bwin + BD_NB) * B;
         ctx->prof_bytes[2] += 32.0 * L.np * B + fb;
         CU(cudaStreamSynchronize(st));
@@ -904,7 +968,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         ctx->ev_kind.clear();
     }
     dim3 gs(std::max(1, std::min(32, (L.n + 255) / 256)), B);
-    k_band_scatter<<<gs, 256, 0, st>>>(L.n, L.np, L.Y, L.d_perm, u_out, g, g_idx);
+    k_band_scatter<<<gs, 256, 0, st>>>(L.n, L.np, L.Y, d_perm, u_out, g, g_idx);
     LAUNCHED();
     return PG_OK;
 }
@@ -913,6 +977,14 @@ extern "C" int pg_phi_batch(pg_ctx* ctx, int level, int B, const double* u_prev,
                             const double* guess, const double* inv_dt, const double* src,
                             double* u_out, const double* g, const int32_t* g_idx,
                             void* stream) {
+    return pg_phi_batch_h(ctx, level, B, u_prev, guess, inv_dt, nullptr, src, u_out, g, g_idx,
+                          stream);
+}
+
+extern "C" int pg_phi_batch_h(pg_ctx* ctx, int level, int B, const double* u_prev,
+                              const double* guess, const double* inv_dt,
+                              const double* inv_dt_host, const double* src, double* u_out,
+                              const double* g, const int32_t* g_idx, void* stream) {
     if (!ctx) return PG_EINVAL;
     if (level < 0 || level >= (int)ctx->levels.size())
         return set_err(ctx, PG_EINVAL, "no spatial level %d", level);
@@ -942,7 +1014,7 @@ extern "C" int pg_phi_batch(pg_ctx* ctx, int level, int B, const double* u_prev,
         LAUNCHED();
         return PG_OK;
     } else if (ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok) {
-        return band_phi(ctx, L, B, u_prev, inv_dt, src, u_out, g, g_idx, st);
+        return band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
     } else if (L.resident) {
         return launch_resident(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st);
     } else if (L.dia) {

@@ -168,6 +168,7 @@ class _Level:
         inv = np.zeros(self.n_points)
         inv[1:] = 1.0 / (t[1:] - t[:-1])                 # dt = t_next - t_prev
         self.inv_dt_all = torch.as_tensor(inv, **f64)
+        self.inv_dt_all_h = inv
         src = [prob.source_values(t, smooth=False), prob.source_values(t, smooth=True)]
         self.src_all = [torch.as_tensor(np.ascontiguousarray(s), **f64) for s in src]
         self.row_of_pt = torch.as_tensor(np.arange(self.n_points) - self.own_lo,
@@ -175,10 +176,12 @@ class _Level:
         self.pt_idx = torch.arange(self.n_points, dtype=torch.int32, device=dev)
         # per F-offset tables (contiguous [K] / [K, n_src])
         self.inv_dt_off, self.src_off, self.gidx_off = {}, [{}, {}], {}
+        self.inv_dt_off_h = {}
         for j in range(1, self.m + 1):
             pts = self.c_idx - self.m + j
             pt = torch.as_tensor(pts, device=dev)
             self.inv_dt_off[j] = self.inv_dt_all[pt].contiguous()
+            self.inv_dt_off_h[j] = np.ascontiguousarray(inv[pts])
             for sm in (0, 1):
                 self.src_off[sm][j] = self.src_all[sm][pt].contiguous()
             self.gidx_off[j] = torch.as_tensor(pts - self.own_lo, dtype=torch.int32,
@@ -222,6 +225,8 @@ class MgritSolver:
             lvl.crhs = torch.zeros(lvl.K, nxt.n, **f64)
         self._plans = {}
         self._smooth = False
+        import inspect
+        self._takes_host_dt = "inv_dt_host" in inspect.signature(problem.phi_batch).parameters
         self.phi_columns = 0
         self.phi_calls = 0
         self.setup_seconds = time.perf_counter() - t_setup
@@ -246,16 +251,22 @@ class MgritSolver:
         use_g = add_rhs and lvl.use_rhs
         self.problem.phi_batch(lvl.s, U, lvl.inv_dt_off[j], lvl.src_off[self._smooth][j], out,
                                g=lvl.rhs if use_g else None,
-                               g_idx=lvl.gidx_off[j] if use_g else None)
+                               g_idx=lvl.gidx_off[j] if use_g else None,
+                               **self._host_dt(lvl.inv_dt_off_h[j]))
         self.phi_columns += U.shape[0]
         self.phi_calls += 1
 
     def _phi_pts(self, lvl, U, lo, hi, out, g=None, g_idx=None):
         """Consecutive points lo..hi-1 of lvl's grid, one column each."""
         self.problem.phi_batch(lvl.s, U, lvl.inv_dt_all[lo:hi],
-                               lvl.src_all[self._smooth][lo:hi], out, g=g, g_idx=g_idx)
+                               lvl.src_all[self._smooth][lo:hi], out, g=g, g_idx=g_idx,
+                               **self._host_dt(lvl.inv_dt_all_h[lo:hi]))
         self.phi_columns += hi - lo
         self.phi_calls += 1
+
+    def _host_dt(self, arr):
+        """host copy of 1/dt for problems that accept it (skips a D2H read)"""
+        return {"inv_dt_host": arr} if self._takes_host_dt else {}
 
     # --- communication (reference mgrit.py:339-357) ---
     def _exchange_left(self, lvl):

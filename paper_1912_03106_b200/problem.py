@@ -181,15 +181,19 @@ class GpuFemProblem:
     def _stream(self):
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
-    def phi_batch(self, level, u_prev, inv_dt, src, out, g=None, g_idx=None, guess=None):
-        """out[b] = Phi(u_prev[b]) (+ g[g_idx[b]]).  All device tensors:
-        u_prev/out [B, n] fp64, inv_dt [B], src [B, n_src], g [*, n], g_idx [B]
-        int32."""
+    def phi_batch(self, level, u_prev, inv_dt, src, out, g=None, g_idx=None, guess=None,
+                  inv_dt_host=None):
+        """out[b] = Phi(u_prev[b]) (+ g[g_idx[b]]).  Device tensors: u_prev/out
+        [B, n] fp64, inv_dt [B], src [B, n_src], g [*, n], g_idx [B] int32;
+        inv_dt_host: optional contiguous fp64 numpy copy of inv_dt."""
         B = int(u_prev.shape[0])
-        rc = self.lib.pg_phi_batch(self.ctx, int(level), B, _lib.ptr(u_prev),
-                                   _lib.ptr(guess), _lib.ptr(inv_dt),
-                                   _lib.ptr(src) if self.n_src else None, _lib.ptr(out),
-                                   _lib.ptr(g), _lib.ptr(g_idx), self._stream())
+        hp = None
+        if inv_dt_host is not None:
+            hp = inv_dt_host.ctypes.data_as(ctypes.c_void_p)
+        rc = self.lib.pg_phi_batch_h(self.ctx, int(level), B, _lib.ptr(u_prev),
+                                     _lib.ptr(guess), _lib.ptr(inv_dt), hp,
+                                     _lib.ptr(src) if self.n_src else None, _lib.ptr(out),
+                                     _lib.ptr(g), _lib.ptr(g_idx), self._stream())
         if rc == _lib.PG_ENEWTON:
             col, its = ctypes.c_int(), ctypes.c_int()
             self.lib.pg_newton_failure(self.ctx, ctypes.byref(col), ctypes.byref(its))
