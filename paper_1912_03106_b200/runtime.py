@@ -131,24 +131,38 @@ class DistTransport:
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
         self.device = device if device is not None else torch.device("cpu")
+        # gloo moves host tensors only: device buffers are staged through the
+        # host (tests run several ranks on one GPU this way); NCCL moves device
+        # tensors directly over NVLink
+        self.stage = dist.get_backend(group) != "nccl" and self.device.type == "cuda"
+        cdev = torch.device("cpu") if self.stage else self.device
+        self.coll_device = cdev
         # the first collective must involve every rank (NCCL p2p rule)
-        t = torch.zeros(1, dtype=torch.float64, device=self.device)
+        t = torch.zeros(1, dtype=torch.float64, device=cdev)
         dist.all_reduce(t, group=group)
 
     def exchange(self, sends, recvs):
         """sends/recvs: lists of (peer, tensor); one grouped p2p batch."""
+        if self.stage:
+            sends = [(peer, t.detach().to("cpu")) for peer, t in sends]
+            staged = [(peer, torch.empty(t.shape, dtype=t.dtype), t) for peer, t in recvs]
+            recvs_h = [(peer, h) for peer, h, _ in staged]
+        else:
+            recvs_h, staged = recvs, []
         ops = [self.dist.P2POp(self.dist.isend, t.contiguous(), peer, self.group)
                for peer, t in sends]
         ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group)
-                for peer, t in recvs]
+                for peer, t in recvs_h]
         if not ops:
             return
         for req in self.dist.batch_isend_irecv(ops):
             req.wait()
+        for _, h, t in staged:
+            t.copy_(h)
 
     def sum_ordered(self, value):
         """Rank-ascending sum of per-rank partials, identical on every rank."""
-        t = torch.tensor([float(value)], dtype=torch.float64, device=self.device)
+        t = torch.tensor([float(value)], dtype=torch.float64, device=self.coll_device)
         out = [torch.zeros_like(t) for _ in range(self.size)]
         self.dist.all_gather(out, t, group=self.group)
         vals = torch.cat(out).cpu().numpy()
@@ -158,7 +172,7 @@ class DistTransport:
         return total
 
     def max(self, value):
-        t = torch.tensor([float(value)], dtype=torch.float64, device=self.device)
+        t = torch.tensor([float(value)], dtype=torch.float64, device=self.coll_device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
 

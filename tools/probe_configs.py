@@ -1,0 +1,45 @@
+"""Time-to-solution of BASELINE configs 1-3 at full size on one GPU (dev tool).
+
+usage: python tools/probe_configs.py cfg1|cfg2|cfg2-direct|cfg3 [max_iters]
+"""
+import json, sys, time
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+from paper_1912_03106_b200 import (GpuFemProblem, CycleSpec, StoppingCriterion, TimeHierarchy,
+                                   build_uniform_grid, MgritSolver, sequential_solve, configs, build)
+build.build()
+name = sys.argv[1]
+max_iters = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+if name == "cfg1":
+    spec = configs.config1()
+elif name == "cfg2":
+    spec = configs.config2(grids=2, strategy="delayed")
+elif name == "cfg2-direct":
+    spec = configs.config2()
+elif name == "cfg3":
+    spec = configs.config3(grids=2, strategy="delayed")
+elif name == "cfg3-window":
+    spec = configs.config3(n_steps=2 ** 10, grids=2, strategy="delayed")
+else:
+    raise SystemExit(name)
+prob = GpuFemProblem(spec)
+mg = spec["mgrit"]
+grid = build_uniform_grid(0.0, spec["tf"] * spec["n_steps"] / 2 ** 14 if name == "cfg3-window" else spec["tf"], spec["n_steps"])
+solver = MgritSolver(prob, TimeHierarchy.build(grid, mg["factors"]),
+                     CycleSpec(kind="V", gamma=1, max_iters=max_iters,
+                               spatial_strategy=mg["spatial_strategy"]),
+                     StoppingCriterion(tolerance=mg["tolerance"]))
+t0 = time.perf_counter()
+run, _ = solver.solve(gather_solution=False)
+torch.cuda.synchronize()
+t = time.perf_counter() - t0
+st = prob.total_stats()
+print(json.dumps({"config": name, "n": prob.spatial.size(0), "n_steps": spec["n_steps"],
+                  "inner": prob.inner, "nonlinear": prob.nonlinear,
+                  "wall_s": t, "solve_s": run.solve_seconds, "iterations": run.iterations,
+                  "converged": run.converged, "failure": run.failure,
+                  "history": [run.initial_residual] + run.residual_norms,
+                  "phi_columns": run.phi_columns, "inner_iters": st["column_iters"],
+                  "newton_iters": st["newton_iters"],
+                  "step_dof_per_s": spec["n_steps"] * prob.spatial.size(0) / t}), flush=True)
