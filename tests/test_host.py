@@ -108,3 +108,15 @@ def test_excitation_table_matches_oracle():
     a = Excitation(**kw).table([1, 2, 3], t)
     b = np.array([[OExc(**kw).value(ph, float(x)) for ph in (1, 2, 3)] for x in t])
     assert np.array_equal(a, b)
+
+
+def test_hierarchy_rejects_levels_without_two_points():
+    """time_hierarchy.py:135-140: a factor leaving < 2 points is an error."""
+    g = build_uniform_grid(0.0, 1.0, 37)
+    with pytest.raises(ValueError):
+        TimeHierarchy.build(g, [4, 4, 4])
+    with pytest.raises(ValueError):
+        TimeHierarchy.build(g, [1])
+    h = TimeHierarchy.build(g, [4, 4])          # 38 -> 10 -> 3 points, F-tails
+    assert [x.n_points for x in h.grids] == [38, 10, 3]
+    assert h.splittings[0].c_indices[-1] == 36 and h.splittings[2].factor == 2
