@@ -72,6 +72,10 @@ typedef struct pg_level_desc {
     const double*  elem_geo;    /* [n_elem][7]: b0 b1 b2 c0 c1 c2 area     */
     const int32_t* node_elem_ptr; /* [n+1] node -> incident iron elements  */
     const int32_t* node_elem;   /* [..] elem * 4 + local vertex            */
+    /* nonlinear levels, inner = PG_INNER_CHOLESKY: stiffness of the
+     * linearised operator (iron at nu(|B| = 0)) on the CSR pattern; its
+     * banded-Cholesky factor preconditions the Newton systems. Nullable. */
+    const double*  k_pre_val;   /* [nnz]                                   */
 } pg_level_desc;
 
 /* Inner-solver and material options (NewtonOptions, problems.py:39-50;
@@ -115,8 +119,10 @@ int  pg_set_options(pg_ctx* ctx, const pg_solver_opts* opts);
  * starting from guess[b] (NULL = u_prev), then adds g[g_idx[b]] when g is
  * non-NULL and g_idx[b] >= 0.  inv_dt: [B]; src: [B][n_src]; g: [*][n];
  * g_idx: [B] int32.  u_out must not alias u_prev or guess.
- * Linear levels: Jacobi-PCG.  Levels with iron elements: damped Newton
- * (problems.py:201-244) with a Jacobi-PCG inner solve; on failure returns
+ * Linear levels: banded Cholesky (PG_INNER_CHOLESKY) or Jacobi-PCG.  Levels
+ * with iron elements: damped Newton (problems.py:201-244), inner solve CG
+ * preconditioned by the banded-Cholesky factor of the linearised operator
+ * (PG_INNER_CHOLESKY, needs k_pre_val) or Jacobi-PCG; on failure returns
  * PG_ENEWTON and pg_newton_failure() reports column and iteration count. */
 int  pg_phi_batch(pg_ctx* ctx, int level, int B,
                   const double* u_prev, const double* guess,

@@ -32,6 +32,7 @@ class LevelDesc(ctypes.Structure):
         ("side", c_int32),
         ("n_elem", c_int32), ("elem_dof", P_int32), ("elem_geo", P_double),
         ("node_elem_ptr", P_int32), ("node_elem", P_int32),
+        ("k_pre_val", P_double),
     ]
 
 

@@ -103,7 +103,10 @@ def config3(N=128, n_steps=2 ** 14, levels=3, carrier="triangle", grids=None,
                       "k3": 3.96e-4,
                       "newton": {"tol": 1e-8, "max_iters": 10, "damping": 0.5,
                                  "max_halvings": 8}}
-    s["inner"].update(kind="pcg", rtol=1e-12)      # config 3: "PCG inner solve"
+    # config 3's "PCG inner solve": CG on the Newton system, preconditioned by
+    # the banded-Cholesky factor of the linearised operator ("cholesky"); the
+    # Jacobi-preconditioned variant is inner kind "pcg"
+    s["inner"].update(kind="cholesky", rtol=1e-12)
     s["name"] = "cfg3"
     return s
 

@@ -433,18 +433,25 @@ k_band_chain1(BandSolveArgs a) {
     }
 }
 
-// Y[gc] = c M u_prev + f  (CSR), padded rows zero
+// Y[gc] = c M u_prev + f  (CSR), or Y[gc] = copy_src[perm[gc]] when
+// copy_src is given (preconditioner applications); padded rows zero
 __global__ void k_band_rhs(int n, int ldy, const int* __restrict__ row_ptr,
                            const int* __restrict__ col_idx, const double* __restrict__ m_val,
                            int n_src, const double* __restrict__ shapes,
                            const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
                            const double* __restrict__ src, const int* __restrict__ perm,
-                           double* __restrict__ Y) {
+                           double* __restrict__ Y, const double* __restrict__ copy_src) {
     const int gc = blockIdx.y;
     const int b = perm[gc];
+    double* y = Y + (size_t)gc * ldy;
+    if (copy_src) {
+        const double* x = copy_src + (size_t)b * n;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ldy; i += gridDim.x * blockDim.x)
+            y[i] = i < n ? x[i] : 0.0;
+        return;
+    }
     const double c = inv_dt[b];
     const double* u = u_prev + (size_t)b * n;
-    double* y = Y + (size_t)gc * ldy;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ldy; i += gridDim.x * blockDim.x) {
         if (i >= n) { y[i] = 0.0; continue; }
         double mu = 0.0;

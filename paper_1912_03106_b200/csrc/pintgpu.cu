@@ -8,6 +8,7 @@
 #include "mgrit_ops.cuh"
 #include "newton.cuh"
 #include "band.cuh"
+#include "newton_nk.cuh"
 
 #include <algorithm>
 #include <cstdarg>
@@ -58,6 +59,14 @@ struct Level {
     // column grouping cache: hash of the inv_dt pattern -> device perm/chunks
     struct Group { std::vector<double> key; int* perm; int4* chunks; int nch; int BC; };
     std::unordered_map<uint64_t, std::vector<Group>> groups;
+    Group tmp_group{};
+    // batched Newton-Krylov workspace
+    double *nk_u = nullptr, *nk_F = nullptr, *nk_D = nullptr, *nk_rhs = nullptr,
+           *nk_R = nullptr, *nk_Z = nullptr, *nk_P = nullptr, *nk_Q = nullptr,
+           *nk_TR = nullptr, *nk_FT = nullptr, *nk_E = nullptr, *nk_ET = nullptr,
+           *nk_s = nullptr;          // per-column scalars [6][B]
+    int* nk_act = nullptr;
+    int nk_B = 0;
     int* d_status = nullptr;
     // nonlinear iron elements
     int n_elem = 0;
@@ -65,6 +74,7 @@ struct Level {
     double* elem_geo = nullptr;
     int* ne_ptr = nullptr;
     int* ne = nullptr;
+    double* k_pre = nullptr;       // linearised stiffness (Newton preconditioner)
     // workspace
     int ws_B = 0;
     PcgWork W{};
@@ -198,7 +208,7 @@ static void free_level(Level& L) {
     void* ptrs[] = {L.row_ptr, L.col_idx, L.m_val, L.k_val, L.dM, L.dK, L.shapes,
                     L.weights, L.tile_lo, L.tile_hi, L.elem_dof, L.elem_geo,
                     L.ne_ptr, L.ne, L.mk, L.d_FL, L.d_FU, L.Y, L.d_perm,
-                    L.d_chunks, L.d_status};
+                    L.d_chunks, L.d_status, L.k_pre};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : L.ws_allocs) cudaFree(p);
@@ -208,6 +218,11 @@ static void free_level(Level& L) {
     for (auto& kv : L.groups)
         for (auto& gr : kv.second) { cudaFree(gr.perm); cudaFree(gr.chunks); }
     L.groups.clear();
+    double* nk[] = {L.nk_u, L.nk_F, L.nk_D, L.nk_rhs, L.nk_R, L.nk_Z, L.nk_P, L.nk_Q,
+                    L.nk_TR, L.nk_FT, L.nk_E, L.nk_ET, L.nk_s};
+    for (double* p : nk)
+        if (p) cudaFree(p);
+    if (L.nk_act) cudaFree(L.nk_act);
 }
 
 extern "C" void pg_destroy(pg_ctx* ctx) {
@@ -394,6 +409,8 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
             (rc = dev_upload(ctx, &L.elem_geo, d->elem_geo, (size_t)d->n_elem * 7)) ||
             (rc = dev_upload(ctx, &L.ne_ptr, d->node_elem_ptr, (size_t)d->n + 1)) ||
             (rc = dev_upload(ctx, &L.ne, d->node_elem, (size_t)nne)))
+            return -1;
+        if (d->k_pre_val && (rc = dev_upload(ctx, &L.k_pre, d->k_pre_val, (size_t)d->nnz)))
             return -1;
     }
     ctx->levels.push_back(L);
@@ -726,6 +743,9 @@ static int begin_stats(pg_ctx* ctx, Level& L, cudaStream_t st) {
 static int newton_batch(pg_ctx* ctx, Level& L, int B, const double* u_prev,
                         const double* guess, const double* inv_dt, const double* src,
                         double* u_out, cudaStream_t st);
+static int newton_nk(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* guess,
+                     const double* inv_dt, const double* inv_dt_host, const double* src,
+                     double* u_out, const double* g, const int* g_idx, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // banded-Cholesky Phi (problems.py:130-146 on the GPU)
@@ -788,7 +808,8 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     CU(cudaMallocAsync(&d_c, nf * sizeof(double), st));
     CU(cudaMemcpyAsync(d_lb, lbs.data(), nf * sizeof(double*), cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_c, cs.data(), nf * sizeof(double), cudaMemcpyHostToDevice, st));
-    BandFactorArgs a{L.n, L.bw, L.bwin, L.LDA, L.nblk, L.row_ptr, L.col_idx, L.m_val, L.k_val};
+    BandFactorArgs a{L.n, L.bw, L.bwin, L.LDA, L.nblk, L.row_ptr, L.col_idx, L.m_val,
+                     L.n_elem > 0 ? L.k_pre : L.k_val};
     dim3 gb(std::min(1024, (L.n + 255) / 256), nf);
     k_band_build<<<gb, 256, 0, st>>>(a, d_c, d_lb);
     LAUNCHED();
@@ -849,11 +870,19 @@ static uint64_t hash_doubles(const double* v, int n) {
     return h;
 }
 
+// Banded-Cholesky solve of B columns.  Default: Phi (rhs = c M u_prev + f,
+// columns 0..B-1).  Preconditioner mode (copy_src != NULL): the rhs of
+// column j is copy_src[sub[j]], the result goes to u_out[sub[j]] (sub: host
+// list of column indices into full-batch arrays).
 static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* inv_dt,
                     const double* inv_dt_host, const double* src, double* u_out,
-                    const double* g, const int* g_idx, cudaStream_t st) {
+                    const double* g, const int* g_idx, cudaStream_t st,
+                    const double* copy_src = nullptr, const int* sub = nullptr) {
     std::vector<double> c(B);
-    if (inv_dt_host) {
+    if (sub) {
+        // preconditioner mode: inv_dt_host is the full-batch host array
+        for (int j = 0; j < B; ++j) c[j] = inv_dt_host[sub[j]];
+    } else if (inv_dt_host) {
         memcpy(c.data(), inv_dt_host, B * sizeof(double));
     } else {
         CU(cudaMemcpyAsync(c.data(), inv_dt, B * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -863,10 +892,11 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     // cached grouping for this exact inv_dt pattern?
     const uint64_t h = hash_doubles(c.data(), B);
     Level::Group* grp = nullptr;
-    for (auto& gr : L.groups[h])
-        if ((int)gr.key.size() == B && gr.BC == BC &&
-            memcmp(gr.key.data(), c.data(), B * sizeof(double)) == 0)
-            grp = &gr;
+    if (!sub)
+        for (auto& gr : L.groups[h])
+            if ((int)gr.key.size() == B && gr.BC == BC &&
+                memcmp(gr.key.data(), c.data(), B * sizeof(double)) == 0)
+                grp = &gr;
     int rc;
     std::vector<int> fid;
     if (!grp) {
@@ -903,14 +933,33 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             chunks.push_back(make_int4(fid[perm[i]], i, j - i, 0));
             i = j;
         }
-        Level::Group gr{c, nullptr, nullptr, (int)chunks.size(), BC};
-        CU(cudaMalloc(&gr.perm, B * sizeof(int)));
-        CU(cudaMalloc(&gr.chunks, chunks.size() * sizeof(int4)));
-        CU(cudaMemcpy(gr.perm, perm.data(), B * sizeof(int), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(gr.chunks, chunks.data(), chunks.size() * sizeof(int4),
-                      cudaMemcpyHostToDevice));
-        L.groups[h].push_back(gr);
-        grp = &L.groups[h].back();
+        if (sub)
+            for (int& x : perm) x = sub[x];
+        if (sub) {
+            // transient grouping (active-column subsets change every call)
+            if (B > L.perm_cap) {
+                if (L.d_perm) cudaFree(L.d_perm);
+                if (L.d_chunks) cudaFree(L.d_chunks);
+                L.perm_cap = std::max(B, 64);
+                CU(cudaMalloc(&L.d_perm, L.perm_cap * sizeof(int)));
+                CU(cudaMalloc(&L.d_chunks, L.perm_cap * sizeof(int4)));
+            }
+            CU(cudaMemcpyAsync(L.d_perm, perm.data(), B * sizeof(int), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(L.d_chunks, chunks.data(), chunks.size() * sizeof(int4),
+                               cudaMemcpyHostToDevice, st));
+            CU(cudaStreamSynchronize(st));       // host vectors go out of scope
+            L.tmp_group = Level::Group{c, L.d_perm, L.d_chunks, (int)chunks.size(), BC};
+            grp = &L.tmp_group;
+        } else {
+            Level::Group gr{c, nullptr, nullptr, (int)chunks.size(), BC};
+            CU(cudaMalloc(&gr.perm, B * sizeof(int)));
+            CU(cudaMalloc(&gr.chunks, chunks.size() * sizeof(int4)));
+            CU(cudaMemcpy(gr.perm, perm.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+            CU(cudaMemcpy(gr.chunks, chunks.data(), chunks.size() * sizeof(int4),
+                          cudaMemcpyHostToDevice));
+            L.groups[h].push_back(gr);
+            grp = &L.groups[h].back();
+        }
     }
     const int* d_perm = grp->perm;
     const int4* d_chunks = grp->chunks;
@@ -922,7 +971,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     }
     dim3 gr(std::max(1, std::min(32, (L.np + 255) / 256)), B);
     k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, L.row_ptr, L.col_idx, L.m_val, L.n_src, L.shapes,
-                                   u_prev, inv_dt, src, d_perm, L.Y);
+                                   u_prev, inv_dt, src, d_perm, L.Y, copy_src);
     LAUNCHED();
     BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL};
     const int nst = band_stages(L, BC);
@@ -1006,6 +1055,9 @@ extern "C" int pg_phi_batch_h(pg_ctx* ctx, int level, int B, const double* u_pre
     int rc = ensure_ws(ctx, L, B);
     if (rc) return rc;
     if ((rc = begin_stats(ctx, L, st))) return rc;
+    if (L.n_elem > 0 && ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok && L.k_pre) {
+        return newton_nk(ctx, L, B, u_prev, guess, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
+    }
     if (L.n_elem > 0) {
         rc = newton_batch(ctx, L, B, u_prev, guess, inv_dt, src, u_out, st);
         if (rc) return rc;

@@ -94,23 +94,28 @@ class GridModel:
         P = N + 1
         Mst = {o: np.zeros((P, P)) for o in OFFSETS}
         Kst = {o: np.zeros((P, P)) for o in OFFSETS}
+        # preconditioner stiffness of the nonlinear model: iron at nu(|B| = 0)
+        Kpre = {o: np.zeros((P, P)) for o in OFFSETS}
+        nu_iron0 = nu0 * (nl["k1"] + nl["k3"]) if nl else nu0
         src_nodes = [np.zeros((P, P)) for _ in phases]
         area = 0.5 * h * h
         for t, (tri, Kref) in enumerate(((TRI_LOWER, K_LOWER), (TRI_UPPER, K_UPPER))):
             msc = sig[t] * h * h                         # (N, N) per cell
             ksc = np.where(iron[t], 0.0, nu0)            # iron handled matrix-free
+            kpc = np.where(iron[t], nu_iron0, nu0)
             for a, (ax, ay) in enumerate(tri):
                 rows = (slice(ay, ay + N), slice(ax, ax + N))
                 for b, (bx, by) in enumerate(tri):
                     off = (bx - ax, by - ay)
                     Mst[off][rows] += msc * M_REF[a, b]
                     Kst[off][rows] += ksc * Kref[a, b]
+                    Kpre[off][rows] += kpc * Kref[a, b]
                 for k in range(len(phases)):
                     src_nodes[k][rows] += inside[t][k] * (area / 3.0)
         # interior rows -> CSR
         m = self.side
         ii, jj = np.meshgrid(np.arange(1, N), np.arange(1, N))   # [j-1, i-1]
-        cols, mv, kv, valid = [], [], [], []
+        cols, mv, kv, kp, valid = [], [], [], [], []
         for (dx, dy) in OFFSETS:
             ni, nj = ii + dx, jj + dy
             ok = (ni >= 1) & (ni <= m) & (nj >= 1) & (nj <= m)
@@ -118,15 +123,18 @@ class GridModel:
             cols.append(((nj - 1) * m + (ni - 1)).reshape(-1))
             mv.append(Mst[(dx, dy)][1:N, 1:N].reshape(-1))
             kv.append(Kst[(dx, dy)][1:N, 1:N].reshape(-1))
+            kp.append(Kpre[(dx, dy)][1:N, 1:N].reshape(-1))
         valid = np.stack(valid, 1)
         cols = np.stack(cols, 1)
         mv = np.stack(mv, 1)
         kv = np.stack(kv, 1)
+        kp = np.stack(kp, 1)
         counts = valid.sum(1)
         self.row_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
         self.col_idx = cols[valid].astype(np.int32)
         self.m_val = np.ascontiguousarray(mv[valid])
         self.k_val = np.ascontiguousarray(kv[valid])
+        self.k_pre = np.ascontiguousarray(kp[valid]) if nl else None
         self.nnz = int(self.row_ptr[-1])
         self.shapes = np.stack([s[1:N, 1:N].reshape(-1) for s in src_nodes]) \
             if phases else np.zeros((0, self.n))

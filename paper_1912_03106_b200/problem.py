@@ -117,6 +117,9 @@ class GpuFemProblem:
             d.elem_geo = _np_ptr(arrays["elem_geo"], ctypes.c_double)
             d.node_elem_ptr = _np_ptr(arrays["node_elem_ptr"], ctypes.c_int32)
             d.node_elem = _np_ptr(arrays["node_elem"], ctypes.c_int32)
+        if getattr(g, "k_pre", None) is not None:
+            arrays["k_pre"] = np.ascontiguousarray(g.k_pre)
+            d.k_pre_val = _np_ptr(arrays["k_pre"], ctypes.c_double)
         idx = self.lib.pg_add_level(self.ctx, ctypes.byref(d))
         if idx < 0:
             _lib.check(self.ctx, _lib.PG_EINVAL, "pg_add_level")

@@ -55,11 +55,13 @@ def test_mgrit_matches_reference_engine(cuda, name, inner):
     assert err < 1e-9, err
 
 
-def test_nonlinear_mgrit_matches_reference_engine(cuda):
-    """Config-3 model (Brauer iron, Newton + PCG) on a 32^2 / 256-step window:
+@pytest.mark.parametrize("inner", ["cholesky", "pcg"])
+def test_nonlinear_mgrit_matches_reference_engine(cuda, inner):
+    """Config-3 model (Brauer iron, Newton) on a 32^2 / 256-step window:
     same iterations as the reference engine, history within 1e-6."""
     fx = load_golden("mgrit_cfg3_delayed_n32")
-    prob, grid, run, sol = _run(fx["spec"], int(fx["max_iters"]), float(fx["tol"]))
+    prob, grid, run, sol = _run(fx["spec"], int(fx["max_iters"]), float(fx["tol"]),
+                                inner=inner)
     hist = np.array([run.initial_residual] + run.residual_norms)
     assert run.iterations == int(fx["iterations"])
     rel = np.abs(hist - fx["history"]) / fx["history"]

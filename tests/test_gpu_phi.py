@@ -50,13 +50,14 @@ def test_phi_batch_matches_oracle(cuda, name, smooth, inner):
         assert err.max() < TOL[inner], (name, g, err.max(), st)
 
 
+@pytest.mark.parametrize("inner", ["cholesky", "pcg"])
 @pytest.mark.parametrize("smooth", [False, True])
-def test_nonlinear_newton_phi_matches_oracle(cuda, smooth):
+def test_nonlinear_newton_phi_matches_oracle(cuda, smooth, inner):
     """Batched damped Newton (problems.py:201-244) with matrix-free element
     Jacobian + Jacobi-PCG vs the oracle's banded-Jacobian Newton; both stop
     at |F| <= 1e-8 |rhs| along the same trajectory."""
     fx = load_golden("phi_cfg3_n32")
-    prob = _problem(fx["spec"])
+    prob = _problem(fx["spec"], inner=inner)
     assert prob.nonlinear
     for g in range(prob.spatial.n_grids):
         ref = fx[f"phis{g}" if smooth else f"phi{g}"]
