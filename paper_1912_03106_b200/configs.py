@@ -114,7 +114,6 @@ def config3(N=128, n_steps=2 ** 14, levels=3, carrier="triangle", grids=None,
 def config4(N=512, n_steps=2 ** 16, levels=4, carrier="triangle", grids=None,
             strategy="direct"):
     s = config2(N, n_steps, levels, carrier, grids, strategy)
-    s["inner"]["kind"] = "pcg"        # bandwidth 512: beyond the band-solve smem window
     s["name"] = "cfg4"
     return s
 

@@ -37,8 +37,17 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // ---------------------------------------------------------------------------
 // factorisation: one CTA per factor, 256 threads
 // LB[i][d] = A[i][i-d] (d = 0..w), A = c M + K built from the CSR (lower part)
+// Solve-operand layout of one block row (doubles): piece 0 = the 32 x 32
+// diagonal-block inverse (row stride BD_PD), then NCHK pieces of CW window
+// columns each (row stride CW + 4): every piece is one contiguous TMA copy.
+#define BD_PD 36
+__host__ __device__ __forceinline__ int bd_cw(int W) { return W < 128 ? W : 128; }
+__host__ __device__ __forceinline__ size_t bd_block_doubles(int W) {
+    return (size_t)32 * (BD_PD + (W / bd_cw(W)) * (bd_cw(W) + 4));
+}
+
 struct BandFactorArgs {
-    int n, w, W, LDA, nblk;     // LDA: row stride of the chain operands (W + 4)
+    int n, w, W, LDA, nblk;     // LDA unused (kept for ABI stability of the struct)
     const int* row_ptr;
     const int* col_idx;
     const double* m_val;
@@ -61,7 +70,7 @@ k_band_build(BandFactorArgs a, const double* __restrict__ cvals, double* const* 
     }
 }
 
-// smem: D[32][33], Dinv[32][33], P[w][33], Lw[32][W]
+// smem: D[32][33], Dinv[32][33], P[w][33], Lw[32][CW] (one window chunk)
 // Per block row k it emits FL[k] = [D_k^-1 | D_k^-1 L_win] and
 // FU[k] = [D_k^-T | D_k^-T U_win] (32 x LDA, LDA = 32 + W + 4): the solve
 // step is y_k = D_k^-1 b_k - (D_k^-1 L_win) y_win, whose first term does not
@@ -156,37 +165,45 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
             const int gr = r0 + r, gc = k0 + j;
             if (j < kb && gr - gc <= a.w) lb(gr, gc) = P[r * S + j];
         }
-        // 5. solve operands of block k
-        //    Lw[i][q] = L[k0+i][k0-W+q] (final: earlier panels)
-        for (int t = tid; t < NB * a.W; t += blockDim.x) {
-            const int i = t / a.W, q = t % a.W;
-            const int gr = k0 + i, gc = k0 - a.W + q;
-            Lw[t] = (i < kb && gc >= 0 && gr - gc <= a.w) ? lb(gr, gc) : 0.0;
-        }
-        __syncthreads();
-        double* fl = FL + (size_t)k * NB * a.LDA;
-        double* fu = FU + (size_t)k * NB * a.LDA;
-        for (int t = tid; t < NB * a.LDA; t += blockDim.x) {
-            const int i = t / a.LDA, j = t % a.LDA;
-            double vl = 0.0, vu = 0.0;
-            if (j < NB) {
-                vl = Di[i * S + j];                 // D^-1
-                vu = Di[j * S + i];                 // D^-T
-            } else if (j < NB + a.W) {
-                const int q = j - NB;
-                // (D^-1 L_win)[i][q] = sum_p Di[i][p] Lw[p][q]
-#pragma unroll 8
-                for (int p = 0; p <= i; ++p) vl = fma(Di[i * S + p], Lw[p * a.W + q], vl);
-                // (D^-T U_win)[i][q] = sum_p Di[p][i] P[q][p]
-                if (q < m) {
-#pragma unroll 8
-                    for (int p = i; p < NB; ++p) vu = fma(Di[p * S + i], P[q * S + p], vu);
-                }
+        // 5. solve operands of block k, piece by piece (layout: bd_block_doubles)
+        {
+            const int CW = bd_cw(a.W), nchk = a.W / CW;
+            double* fl = FL + (size_t)k * bd_block_doubles(a.W);
+            double* fu = FU + (size_t)k * bd_block_doubles(a.W);
+            for (int t = tid; t < NB * BD_PD; t += blockDim.x) {
+                const int i = t / BD_PD, j = t % BD_PD;
+                fl[t] = j < NB ? Di[i * S + j] : 0.0;              // D^-1
+                fu[t] = j < NB ? Di[j * S + i] : 0.0;              // D^-T
             }
-            fl[t] = vl;
-            fu[t] = vu;
+            for (int c = 0; c < nchk; ++c) {
+                // Lw[i][q] = L[k0+i][k0-W+c CW+q] (final: earlier panels)
+                for (int t = tid; t < NB * CW; t += blockDim.x) {
+                    const int i = t / CW, q = c * CW + t % CW;
+                    const int gr = k0 + i, gc = k0 - a.W + q;
+                    Lw[t] = (i < kb && gc >= 0 && gr - gc <= a.w) ? lb(gr, gc) : 0.0;
+                }
+                __syncthreads();
+                double* flc = fl + NB * BD_PD + (size_t)c * NB * (CW + 4);
+                double* fuc = fu + NB * BD_PD + (size_t)c * NB * (CW + 4);
+                for (int t = tid; t < NB * (CW + 4); t += blockDim.x) {
+                    const int i = t / (CW + 4), ql = t % (CW + 4), q = c * CW + ql;
+                    double vl = 0.0, vu = 0.0;
+                    if (ql < CW) {
+                        // (D^-1 L_win)[i][q] = sum_p Di[i][p] Lw[p][q]
+#pragma unroll 8
+                        for (int p = 0; p <= i; ++p) vl = fma(Di[i * S + p], Lw[p * CW + ql], vl);
+                        // (D^-T U_win)[i][q] = sum_p Di[p][i] P[q][p]
+                        if (q < m) {
+#pragma unroll 8
+                            for (int p = i; p < NB; ++p) vu = fma(Di[p * S + i], P[q * S + p], vu);
+                        }
+                    }
+                    flc[t] = vl;
+                    fuc[t] = vu;
+                }
+                __syncthreads();
+            }
         }
-        __syncthreads();
         // 6. trailing update of the band: A[r][s] -= P[r] . P[s], s <= r
         for (int t = tid; t < m * m; t += blockDim.x) {
             const int r = t / m, s = t % m;
@@ -202,29 +219,32 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
 
 // ---------------------------------------------------------------------------
 // batched solves
-#define BD_MAXST 2
-constexpr int NST = 2;           // TMA ring depth (see band_stages)
 struct BandSolveArgs {
     int np, W, LDA, nblk, ldy;
-    int nst;                     // TMA ring depth (2..BD_MAXST)
+    int nst;                     // unused
     double* Y;                   // [n_cols][ldy] grouped columns, in place
     const int4* chunks;          // (factor, first grouped column, count, 0)
     double* const* F;            // per factor: FL or FU base (chain operands)
 };
 
-// The sequential chain:  y_k = D_k^-1 b_k - (D_k^-1 L_win) y_window.
+// The sequential chain:  y_k = D_k^-1 b_k - (D_k^-1 L_win) y_window
+// (backward: D^-T, U_win), for windows W <= 256 (whole block <= 77 KB).
 // 4 warps, warp w owns rows 8w..8w+7.  Per block step: one DMMA chain for
 // D_k^-1 b_k (b_k staged in smem one step ahead -- independent of the
 // window) plus NCH chains over the window, a single barrier.  The next
 // block's operands arrive by TMA (2-stage mbarrier ring); the window is a
 // shared-memory ring holding the last 2*NSLOT blocks.
-// smem (doubles): stage[2][NB * LDA], ring[2 NSLOT][NB][BC + 4], sb[2][NB][BC + 4]
+// smem (doubles): stage[2][block], ring[2 NSLOT][NB][BC + 4], sb[2][NB][BC + 4]
 #define BD_CT 128
-template <int BC, int NSLOT, bool FWD>
+#define BD_NST 2
+template <int BC, int CW, int NCHK, bool FWD>
 __global__ void __launch_bounds__(BD_CT)
 k_band_chain(BandSolveArgs a) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ __align__(8) uint64_t bar[BD_MAXST];
+    __shared__ __align__(8) uint64_t bar[BD_NST];
+    constexpr int NST = BD_NST;
+    constexpr int NSLOT = CW * NCHK / BD_NB;
+    constexpr int BLK = BD_NB * (BD_PD + NCHK * (CW + 4));
     const int4 ch = a.chunks[blockIdx.x];
     const double* F = a.F[ch.x];
     const int col0 = ch.y, ncol = ch.z;
@@ -233,12 +253,12 @@ k_band_chain(BandSolveArgs a) {
     constexpr int NCH = W >= 128 ? 8 : 4;
     constexpr int RMASK = 2 * NSLOT - 1;
     double* stage = sm;
-    double* ring = stage + (size_t)NST * NB * a.LDA;
+    double* ring = stage + (size_t)NST * BLK;
     double* sb = ring + (size_t)2 * NSLOT * NB * RS;   // [2][NB][RS]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q4 = lane & 3;
     const int lrow = 8 * warp + g;
-    const uint32_t blk_bytes = (uint32_t)(NB * a.LDA * 8);
+    const uint32_t blk_bytes = (uint32_t)(BLK * 8);
     // b staging: thread t moves (row t & 31, columns (t >> 5) + 4 j)
     constexpr int BPT = BC / 4;
     const int brow = threadIdx.x & 31, bcol = threadIdx.x >> 5;
@@ -269,7 +289,7 @@ k_band_chain(BandSolveArgs a) {
     if (threadIdx.x == 0) {
         for (int q = 0; q + 1 < NST && q < a.nblk; ++q) {
             mbar_arrive_expect_tx(&bar[q], blk_bytes);
-            tma_load_1d(stage + (size_t)q * NB * a.LDA, F + (size_t)blk_of(q) * NB * a.LDA,
+            tma_load_1d(stage + (size_t)q * BLK, F + (size_t)blk_of(q) * BLK,
                         blk_bytes, &bar[q]);
         }
     }
@@ -283,8 +303,8 @@ k_band_chain(BandSolveArgs a) {
             const int sn = (s + 1) & 1;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[sn], blk_bytes);
-            tma_load_1d(stage + (size_t)sn * NB * a.LDA,
-                        F + (size_t)blk_of(s + NST - 1) * NB * a.LDA, blk_bytes, &bar[sn]);
+            tma_load_1d(stage + (size_t)sn * BLK,
+                        F + (size_t)blk_of(s + NST - 1) * BLK, blk_bytes, &bar[sn]);
         }
         // b of block s+1 (in registers since the previous step) -> smem; prefetch s+2
         if (s + 1 < a.nblk) {
@@ -302,7 +322,8 @@ k_band_chain(BandSolveArgs a) {
             for (int nt = 0; nt < NT8; ++nt) dacc[c][nt][0] = dacc[c][nt][1] = 0.0;
         const int row = NB * k + lrow;
         mbar_wait(&bar[st], (s >> 1) & 1);
-        const double* Lrow = stage + (size_t)st * NB * a.LDA + lrow * a.LDA;
+        const double* Lst = stage + (size_t)st * BLK;
+        const double* Lrow = Lst + lrow * BD_PD;
         // D_k^-1 b_k  (independent of the window)
         const double* bb = sb + (size_t)sb_cur * NB * RS;
 #pragma unroll
@@ -320,7 +341,8 @@ k_band_chain(BandSolveArgs a) {
             const int blk = FWD ? (k - NSLOT + wbi) : (k + 1 + wbi);
             const bool ok = FWD ? (blk >= 0) : (blk < a.nblk);
             const int slot = blk & RMASK;
-            const double av = -Lrow[NB + j + q4];
+            const double av = -Lst[NB * BD_PD + (j / CW) * NB * (CW + 4) + lrow * (CW + 4) +
+                                   (j % CW) + q4];
             const double* rr = ring + ((size_t)slot * NB + (j % NB) + q4) * RS + g;
 #pragma unroll
             for (int nt = 0; nt < NT8; ++nt) {
@@ -349,11 +371,14 @@ k_band_chain(BandSolveArgs a) {
 // each lane a quarter of the K = 32 + W dot product with plain fp64 FMAs in
 // two accumulators, reduced by two shuffles; one barrier per block step.
 // smem (doubles): stage[2][NB * LDA], ring[2 NSLOT][NB], sb[2][NB]
-template <int NSLOT, bool FWD>
+template <int CW, int NCHK, bool FWD>
 __global__ void __launch_bounds__(BD_CT)
 k_band_chain1(BandSolveArgs a) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ __align__(8) uint64_t bar[BD_MAXST];
+    __shared__ __align__(8) uint64_t bar[BD_NST];
+    constexpr int NST = BD_NST;
+    constexpr int NSLOT = CW * NCHK / BD_NB;
+    constexpr int BLK = BD_NB * (BD_PD + NCHK * (CW + 4));
     const int4 ch = a.chunks[blockIdx.x];
     const double* F = a.F[ch.x];
     const int col = ch.y;
@@ -361,10 +386,10 @@ k_band_chain1(BandSolveArgs a) {
     constexpr int W = NSLOT * NB;
     constexpr int RMASK = 2 * NSLOT - 1;
     double* stage = sm;
-    double* ring = stage + (size_t)NST * NB * a.LDA;
+    double* ring = stage + (size_t)NST * BLK;
     double* sb = ring + 2 * NSLOT * NB;
     const int r = threadIdx.x >> 2, sub = threadIdx.x & 3;
-    const uint32_t blk_bytes = (uint32_t)(NB * a.LDA * 8);
+    const uint32_t blk_bytes = (uint32_t)(BLK * 8);
     double* Ycol = a.Y + (size_t)col * a.ldy;
 
     for (int t = threadIdx.x; t < 2 * NSLOT * NB; t += BD_CT) ring[t] = 0.0;
@@ -380,7 +405,7 @@ k_band_chain1(BandSolveArgs a) {
     if (threadIdx.x == 0) {
         for (int q = 0; q + 1 < NST && q < a.nblk; ++q) {
             mbar_arrive_expect_tx(&bar[q], blk_bytes);
-            tma_load_1d(stage + (size_t)q * NB * a.LDA, F + (size_t)blk_of(q) * NB * a.LDA,
+            tma_load_1d(stage + (size_t)q * BLK, F + (size_t)blk_of(q) * BLK,
                         blk_bytes, &bar[q]);
         }
     }
@@ -394,15 +419,16 @@ k_band_chain1(BandSolveArgs a) {
             const int sn = (s + 1) & 1;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[sn], blk_bytes);
-            tma_load_1d(stage + (size_t)sn * NB * a.LDA,
-                        F + (size_t)blk_of(s + NST - 1) * NB * a.LDA, blk_bytes, &bar[sn]);
+            tma_load_1d(stage + (size_t)sn * BLK,
+                        F + (size_t)blk_of(s + NST - 1) * BLK, blk_bytes, &bar[sn]);
         }
         if (threadIdx.x < NB && s + 1 < a.nblk) {
             sb[(sb_cur ^ 1) * NB + threadIdx.x] = breg;
             if (s + 2 < a.nblk) breg = Ycol[NB * blk_of(s + 2) + threadIdx.x];
         }
         mbar_wait(&bar[st], (s >> 1) & 1);
-        const double* Lrow = stage + (size_t)st * NB * a.LDA + r * a.LDA;
+        const double* Lst = stage + (size_t)st * BLK;
+        const double* Lrow = Lst + r * BD_PD;
         const double* bb = sb + sb_cur * NB;
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -419,8 +445,9 @@ k_band_chain1(BandSolveArgs a) {
             const bool ok1 = FWD ? (b1 >= 0) : (b1 < a.nblk);
             const double w0 = ok0 ? ring[(b0 & RMASK) * NB + (j % NB)] : 0.0;
             const double w1 = ok1 ? ring[(b1 & RMASK) * NB + ((j + 4) % NB)] : 0.0;
-            a0 = fma(-Lrow[NB + j], w0, a0);
-            a1 = fma(-Lrow[NB + j + 4], w1, a1);
+            const double* Lw = Lst + NB * BD_PD + r * (CW + 4);
+            a0 = fma(-Lw[(j / CW) * NB * (CW + 4) + j % CW], w0, a0);
+            a1 = fma(-Lw[((j + 4) / CW) * NB * (CW + 4) + (j + 4) % CW], w1, a1);
         }
         double v = a0 + a1;
         v += __shfl_xor_sync(0xffffffffu, v, 1);
@@ -430,6 +457,211 @@ k_band_chain1(BandSolveArgs a) {
             Ycol[NB * k + r] = v;
         }
         __syncthreads();
+    }
+}
+
+// The 512-wide window (511^2 grid; 140 KB of operands per block, two
+// blocks no longer fit in smem).  Warp-specialised pipeline: warp 4 is a TMA
+// producer streaming the block operands piece by piece (D^-1, then CW-column
+// window chunks) through a ring of BD_NBUF buffers with full / empty
+// mbarriers, so operand bandwidth overlaps compute for any window width (the
+// 512-wide window of the 511^2 grid is 140 KB per block).  Warps 0-3 consume:
+//   BC >= 8: warp w owns rows 8w..8w+7, fp64 tensor-core MMAs (m8n8k4,
+//            SASS DMMA), NACC independent accumulator chains;
+//   BC == 1: 32 rows x 4 lanes, plain fp64 FMAs, two shuffles.
+// The window lives in a smem ring of NSLOT + 1 slots (block b in slot
+// b mod (NSLOT + 1): never the slot the current window reads), b_k is
+// staged in smem one step ahead; one named barrier (128 consumer threads)
+// per block step.
+#define BD_PCT 160
+#define BD_NBUF 4
+template <int BC, int CW, int NCHK, bool FWD>
+__global__ void __launch_bounds__(BD_PCT)
+k_band_pipe(BandSolveArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t full[BD_NBUF], empty[BD_NBUF];
+    const int4 ch = a.chunks[blockIdx.x];
+    const double* F = a.F[ch.x];
+    const int col0 = ch.y, ncol = ch.z;
+    constexpr int NB = 32;
+    constexpr int W = CW * NCHK;
+    constexpr int NSLOT = W / NB;
+    constexpr int NR = NSLOT + 1;
+    constexpr int RS = BC == 1 ? 1 : BC + 4;
+    constexpr int NT8 = BC >= 8 ? BC / 8 : 1;
+    constexpr int NACC = W >= 128 ? 8 : 4;
+    constexpr int PIECE = NB * (CW + 4) > NB * BD_PD ? NB * (CW + 4) : NB * BD_PD;
+    constexpr int NPB = 1 + NCHK;                      // pieces per block
+    const size_t blk_doubles = (size_t)NB * (BD_PD + NCHK * (CW + 4));
+    double* bufs = sm;
+    double* ring = bufs + (size_t)BD_NBUF * PIECE;
+    double* sb = ring + (size_t)NR * NB * RS;          // [2][NB][RS]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto blk_of = [&](int s) { return FWD ? s : a.nblk - 1 - s; };
+
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < BD_NBUF; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], 4);
+        }
+        mbar_fence_init();
+    }
+    for (int t = threadIdx.x; t < NR * NB * RS; t += BD_PCT) ring[t] = 0.0;
+    __syncthreads();
+
+    if (warp == 4) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            const int total = a.nblk * NPB;
+            for (int P = 0; P < total; ++P) {
+                const int buf = P % BD_NBUF, use = P / BD_NBUF;
+                if (use > 0) mbar_wait(&empty[buf], (use - 1) & 1);
+                const int s = P / NPB, j = P % NPB;
+                const double* src = F + (size_t)blk_of(s) * blk_doubles +
+                                    (j == 0 ? 0 : (size_t)NB * BD_PD + (size_t)(j - 1) * NB * (CW + 4));
+                const uint32_t bytes = (uint32_t)((j == 0 ? NB * BD_PD : NB * (CW + 4)) * 8);
+                mbar_arrive_expect_tx(&full[buf], bytes);
+                tma_load_1d(bufs + (size_t)buf * PIECE, src, bytes, &full[buf]);
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers (warps 0..3) ----------------
+    const int g = lane >> 2, q4 = lane & 3;
+    const int lrow = 8 * warp + g;                      // DMMA row
+    const int r1 = threadIdx.x >> 2, sub = threadIdx.x & 3;   // FMA row / lane
+    double* Ycol0 = a.Y + (size_t)col0 * a.ldy;
+    // b staging: thread t moves row t & 31 of columns (t >> 5) + 4 i
+    constexpr int BPT = BC == 1 ? 1 : BC / 4;
+    const int brow = threadIdx.x & 31, bcol = threadIdx.x >> 5;
+    double breg[BPT];
+    auto load_b = [&](int s) {
+        const int rr = NB * blk_of(s) + brow;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            const int cc = bcol + 4 * i;
+            breg[i] = (BC == 1 ? bcol == 0 : cc < ncol)
+                          ? a.Y[(size_t)(col0 + (BC == 1 ? 0 : cc)) * a.ldy + rr] : 0.0;
+        }
+    };
+    auto store_b = [&](int bufi) {
+#pragma unroll
+        for (int i = 0; i < BPT; ++i)
+            if (BC > 1 || bcol == 0) sb[((size_t)bufi * NB + brow) * RS + (BC == 1 ? 0 : bcol + 4 * i)] = breg[i];
+    };
+    load_b(0);
+    store_b(0);
+    if (a.nblk > 1) load_b(1);
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+
+    for (int s = 0; s < a.nblk; ++s) {
+        const int k = blk_of(s);
+        const int sbc = s & 1;
+        if (s + 1 < a.nblk) {
+            store_b(sbc ^ 1);
+            if (s + 2 < a.nblk) load_b(s + 2);
+        }
+        // window slot of window block 0 and validity
+        const int blk0 = FWD ? (k - NSLOT) : (k + 1);
+        const int slot0 = ((blk0 % NR) + NR) % NR;
+        double acc[NACC][NT8][2];
+#pragma unroll
+        for (int c = 0; c < NACC; ++c)
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
+        double f0 = 0.0, f1 = 0.0;                      // BC == 1 accumulators
+        const double* bb = sb + (size_t)sbc * NB * RS;
+        for (int j = 0; j < NPB; ++j) {
+            const int P = s * NPB + j;
+            const int buf = P % BD_NBUF;
+            mbar_wait(&full[buf], (P / BD_NBUF) & 1);
+            const double* pc = bufs + (size_t)buf * PIECE;
+            if (j == 0) {
+                // D^-1 b_k  (piece 0, row stride BD_PD)
+                if (BC == 1) {
+                    const double* Lr = pc + r1 * BD_PD;
+#pragma unroll
+                    for (int q = sub; q < NB; q += 8) {
+                        f0 = fma(Lr[q], bb[q], f0);
+                        f1 = fma(Lr[q + 4], bb[q + 4], f1);
+                    }
+                } else {
+                    const double* Lr = pc + lrow * BD_PD;
+#pragma unroll
+                    for (int q = 0; q < NB; q += 4) {
+                        const double av = Lr[q + q4];
+                        const double* rr = bb + (q + q4) * RS + g;
+#pragma unroll
+                        for (int nt = 0; nt < NT8; ++nt)
+                            dmma_8x8x4(acc[(q >> 2) % NACC][nt][0], acc[(q >> 2) % NACC][nt][1],
+                                       av, rr[8 * nt]);
+                    }
+                }
+            } else {
+                const int jc = j - 1;                   // window chunk
+                if (BC == 1) {
+                    const double* Lr = pc + r1 * (CW + 4);
+#pragma unroll 4
+                    for (int q = sub; q < CW; q += 8) {
+                        const int jg0 = jc * CW + q, jg1 = jg0 + 4;
+                        const int wb0 = jg0 / NB, wb1 = jg1 / NB;
+                        const bool ok0 = FWD ? (blk0 + wb0 >= 0) : (blk0 + wb0 < a.nblk);
+                        const bool ok1 = FWD ? (blk0 + wb1 >= 0) : (blk0 + wb1 < a.nblk);
+                        int sl0 = slot0 + wb0; if (sl0 >= NR) sl0 -= NR;
+                        int sl1 = slot0 + wb1; if (sl1 >= NR) sl1 -= NR;
+                        const double w0 = ok0 ? ring[sl0 * NB + (jg0 % NB)] : 0.0;
+                        const double w1 = ok1 ? ring[sl1 * NB + (jg1 % NB)] : 0.0;
+                        f0 = fma(-Lr[q], w0, f0);
+                        f1 = fma(-Lr[q + 4], w1, f1);
+                    }
+                } else {
+                    const double* Lr = pc + lrow * (CW + 4);
+#pragma unroll
+                    for (int q = 0; q < CW; q += 4) {
+                        const int jg = jc * CW + q;     // window row (multiple of 4)
+                        const int wb = jg / NB;
+                        const bool ok = FWD ? (blk0 + wb >= 0) : (blk0 + wb < a.nblk);
+                        int sl = slot0 + wb; if (sl >= NR) sl -= NR;
+                        const double av = -Lr[q + q4];
+                        const double* rr = ring + ((size_t)sl * NB + (jg % NB) + q4) * RS + g;
+#pragma unroll
+                        for (int nt = 0; nt < NT8; ++nt) {
+                            const double bv = ok ? rr[8 * nt] : 0.0;
+                            dmma_8x8x4(acc[(q >> 2) % NACC][nt][0], acc[(q >> 2) % NACC][nt][1],
+                                       av, bv);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[buf]);
+        }
+        // combine, store into the ring slot of block k and to global
+        double* slotp = ring + (size_t)(k % NR) * NB * RS;
+        if (BC == 1) {
+            double v = f0 + f1;
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            if (sub == 0) {
+                slotp[r1] = v;
+                Ycol0[NB * k + r1] = v;
+            }
+        } else {
+            const int row = NB * k + lrow;
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cc = 8 * nt + 2 * q4 + h;
+                    double v = 0.0;
+#pragma unroll
+                    for (int c = 0; c < NACC; ++c) v += acc[c][nt][h];
+                    slotp[lrow * RS + cc] = v;
+                    if (cc < ncol) a.Y[(size_t)(col0 + cc) * a.ldy + row] = v;
+                }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // block k visible; sb free
     }
 }
 

@@ -289,11 +289,13 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
     for (int i = 0; i < d->n; ++i)
         for (int e = d->row_ptr[i]; e < d->row_ptr[i + 1]; ++e)
             L.bw = std::max(L.bw, i - d->col_idx[e]);
-    L.bwin = std::max(BD_NB, (L.bw + BD_NB - 1) / BD_NB * BD_NB);
-    L.LDA = BD_NB + L.bwin + 4;
+    // window: the smallest supported width (32 .. 512, powers of two) >= bw
+    L.bwin = BD_NB;
+    while (L.bwin < L.bw && L.bwin < 1024) L.bwin *= 2;
+    L.LDA = (int)(bd_block_doubles(L.bwin) / BD_NB);   // doubles per block row
     L.nblk = (d->n + BD_NB - 1) / BD_NB;
     L.np = L.nblk * BD_NB;
-    L.band_ok = (L.bwin == 32 || L.bwin == 64 || L.bwin == 128 || L.bwin == 256);
+    L.band_ok = L.bwin <= 512;
     // rows per tile: 1024 (4 rows per thread); halo from the CSR
     L.R = 1024;
     L.n_tiles = (d->n + L.R - 1) / L.R;
@@ -752,25 +754,23 @@ static int newton_nk(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
 // columns per solve CTA: 8 (one DMMA n-tile) so a batch of B columns spreads
 // over ~B/8 SMs; 16 when the batch is large enough to fill the GPU anyway.
 static int band_solve_bc(const Level& L, int B, int n_sm) {
-    (void)L;
     if (B <= n_sm) return 1;          // one column per CTA: FMA chain
+    if (L.bwin >= 512) return 8;      // 17-slot window ring leaves room for 8
     return B >= 16 * n_sm ? 16 : 8;
 }
 
-static size_t band_solve_smem(const Level& L, int BC, int nst) {
-    if (BC == 1)
-        return (size_t)(nst * BD_NB * L.LDA + 2 * L.bwin + 2 * BD_NB) * sizeof(double);
-    return (size_t)(nst * BD_NB * L.LDA + 2 * (L.bwin / BD_NB) * BD_NB * (BC + 4) +
-                    2 * BD_NB * (BC + 4)) * sizeof(double);
-}
-
-// TMA ring depth.  Measured (round 1): 2 stages beat 3-4 -- the chain is
-// bound by shared-memory traffic of the 42 KB factor block per step, and
-// more blocks in flight only add smem write pressure.
-static int band_stages(const Level& L, int BC) {
-    (void)L;
-    (void)BC;
-    return 2;
+// smem of the pipelined chain: BD_NBUF operand pieces + (NSLOT+1)-slot
+// window ring + double-buffered b
+static size_t band_solve_smem(const Level& L, int BC) {
+    const int rs = BC == 1 ? 1 : BC + 4;
+    if (L.bwin <= 256)          // whole-block TMA, 2 stages, 2 NSLOT ring
+        return (BD_NST * bd_block_doubles(L.bwin) + (size_t)2 * (L.bwin / BD_NB) * BD_NB * rs +
+                2 * (size_t)BD_NB * rs) * sizeof(double);
+    // pipelined: BD_NBUF operand pieces + (NSLOT+1)-slot ring + 2 b buffers
+    const int cw = bd_cw(L.bwin);
+    const size_t piece = (size_t)BD_NB * std::max(cw + 4, BD_PD);
+    return (BD_NBUF * piece + (size_t)(L.bwin / BD_NB + 1) * BD_NB * rs +
+            2 * (size_t)BD_NB * rs) * sizeof(double);
 }
 
 static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
@@ -778,7 +778,7 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     const int nf = (int)cs.size();
     if (!nf) return PG_OK;
     const int first = (int)L.FL.size();
-    const size_t fbytes = (size_t)L.nblk * BD_NB * L.LDA * sizeof(double);
+    const size_t fbytes = (size_t)L.nblk * bd_block_doubles(L.bwin) * sizeof(double);
     for (int f = 0; f < nf; ++f) {
         double *fl = nullptr, *fu = nullptr;
         CU(cudaMalloc(&fl, fbytes));
@@ -813,8 +813,8 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     dim3 gb(std::min(1024, (L.n + 255) / 256), nf);
     k_band_build<<<gb, 256, 0, st>>>(a, d_c, d_lb);
     LAUNCHED();
-    const size_t sm = (size_t)(2 * BD_NB * (BD_NB + 1) + L.bw * (BD_NB + 1) + BD_NB * L.bwin) *
-                      sizeof(double);
+    const size_t sm = (size_t)(2 * BD_NB * (BD_NB + 1) + L.bw * (BD_NB + 1) +
+                               BD_NB * bd_cw(L.bwin)) * sizeof(double);
     CU(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_band_factor<<<nf, 256, sm, st>>>(a, d_lb, L.d_FL + first, L.d_FU + first, L.d_status);
     LAUNCHED();
@@ -829,34 +829,40 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     return PG_OK;
 }
 
-template <int NS>
-static int launch_band1(pg_ctx* ctx, BandSolveArgs sa, double** d_FU, int nch, size_t sm,
-                        cudaStream_t st) {
-    CU(cudaFuncSetAttribute(k_band_chain1<NS, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CU(cudaFuncSetAttribute(k_band_chain1<NS, false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_band_chain1<NS, true><<<nch, BD_CT, sm, st>>>(sa);
+template <typename KF, typename KB>
+static int launch_pair(pg_ctx* ctx, KF kf, KB kb, int threads, BandSolveArgs sa, double** d_FU,
+                       int nch, size_t sm, cudaStream_t st) {
+    CU(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CU(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kf<<<nch, threads, sm, st>>>(sa);     // L y = b
     LAUNCHED();
     sa.F = d_FU;
-    k_band_chain1<NS, false><<<nch, BD_CT, sm, st>>>(sa);
+    kb<<<nch, threads, sm, st>>>(sa);     // L^T x = y
     LAUNCHED();
     return PG_OK;
 }
 
-template <int BC, int NS>
+template <int BC, int CW, int NCHK>
 static int launch_band(pg_ctx* ctx, BandSolveArgs sa, double** d_FU, int nch, size_t sm,
                        cudaStream_t st) {
-    CU(cudaFuncSetAttribute(k_band_chain<BC, NS, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CU(cudaFuncSetAttribute(k_band_chain<BC, NS, false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_band_chain<BC, NS, true><<<nch, BD_CT, sm, st>>>(sa);     // L y = b
-    LAUNCHED();
-    sa.F = d_FU;
-    k_band_chain<BC, NS, false><<<nch, BD_CT, sm, st>>>(sa);    // L^T x = y
-    LAUNCHED();
-    return PG_OK;
+    if constexpr (CW * NCHK > 256)
+        return launch_pair(ctx, k_band_pipe<BC, CW, NCHK, true>, k_band_pipe<BC, CW, NCHK, false>,
+                           BD_PCT, sa, d_FU, nch, sm, st);
+    else if constexpr (BC == 1)
+        return launch_pair(ctx, k_band_chain1<CW, NCHK, true>, k_band_chain1<CW, NCHK, false>,
+                           BD_CT, sa, d_FU, nch, sm, st);
+    else
+        return launch_pair(ctx, k_band_chain<BC, CW, NCHK, true>,
+                           k_band_chain<BC, CW, NCHK, false>, BD_CT, sa, d_FU, nch, sm, st);
+}
+
+template <int CW, int NCHK>
+static int launch_band_w(pg_ctx* ctx, int BC, BandSolveArgs sa, double** d_FU, int nch,
+                         size_t sm, cudaStream_t st) {
+    if (BC == 1) return launch_band<1, CW, NCHK>(ctx, sa, d_FU, nch, sm, st);
+    if (BC == 8) return launch_band<8, CW, NCHK>(ctx, sa, d_FU, nch, sm, st);
+    if constexpr (CW * NCHK <= 256) return launch_band<16, CW, NCHK>(ctx, sa, d_FU, nch, sm, st);
+    return set_err(ctx, PG_EINVAL, "band batch width %d not supported", BC);
 }
 
 static uint64_t hash_doubles(const double* v, int n) {
@@ -974,22 +980,15 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
                                    u_prev, inv_dt, src, d_perm, L.Y, copy_src);
     LAUNCHED();
     BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL};
-    const int nst = band_stages(L, BC);
-    const size_t sm = band_solve_smem(L, BC, nst);
-    sa.nst = std::max(2, std::min(nst, L.nblk));
+    const size_t sm = band_solve_smem(L, BC);
+    sa.nst = 0;
     if ((rc = prof_mark(ctx, 2, st))) return rc;
-    switch (L.bwin / BD_NB) {
-#define PG_BAND_CASE(NS)                                                                  \
-    case NS:                                                                              \
-        if (BC == 1) rc = launch_band1<NS>(ctx, sa, L.d_FU, nch, sm, st);                \
-        else if (BC == 8) rc = launch_band<8, NS>(ctx, sa, L.d_FU, nch, sm, st);         \
-        else rc = launch_band<16, NS>(ctx, sa, L.d_FU, nch, sm, st);                     \
-        break;
-        PG_BAND_CASE(1)
-        PG_BAND_CASE(2)
-        PG_BAND_CASE(4)
-        PG_BAND_CASE(8)
-#undef PG_BAND_CASE
+    switch (L.bwin) {
+        case 32: rc = launch_band_w<32, 1>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
+        case 64: rc = launch_band_w<64, 1>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
+        case 128: rc = launch_band_w<128, 1>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
+        case 256: rc = launch_band_w<128, 2>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
+        case 512: rc = launch_band_w<128, 4>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
         default: return set_err(ctx, PG_EINVAL, "band window %d not supported", L.bwin);
     }
     if (rc) return rc;
@@ -1003,7 +1002,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         CU(cudaMemcpy(hch.data(), d_chunks, nch * sizeof(int4), cudaMemcpyDeviceToHost));
         for (const int4& q : hch) used[q.x] = 1;
         double fb = 0.0;
-        for (char u : used) fb += u ? 2.0 * L.LDA * L.nblk * BD_NB * 8.0 : 0.0;
+        for (char u : used) fb += u ? 2.0 * bd_block_doubles(L.bwin) * L.nblk * 8.0 : 0.0;
         ctx->prof_flops[2] += 4.0 * L.np * (double)(L.bwin + BD_NB) * B;
         ctx->prof_bytes[2] += 32.0 * L.np * B + fb;
         CU(cudaStreamSynchronize(st));

@@ -180,3 +180,43 @@ def test_residual_and_fas_kernels(cuda):
     rres = torch.empty_like(kept)
     prob.restrict(0, res, rres)
     assert torch.equal(rhs, (kept - cprop) + rres)
+
+
+@pytest.mark.parametrize("N,B", [(300, 150), (512, 3)])
+def test_cholesky_wide_band(cuda, N, B):
+    """Windows of 512 (config 4's 511^2 grid; N = 300 also lands on the
+    512 window): the warp-specialised operand pipeline, with the one-column
+    chain (B <= #SMs) and the 8-column DMMA chain (B > #SMs), vs a sparse
+    direct solve of the oracle's independently assembled operator."""
+    import scipy.sparse.linalg as spla
+    from oracle import fem2d
+    from paper_1912_03106_b200 import configs
+    spec = configs.config4(N=N)
+    spec["n_spatial_grids"] = 1
+    prob = _problem(spec, inner="cholesky")
+    n = prob.spatial.size(0)
+    if B > 1:
+        B = max(B, torch.cuda.get_device_properties(0).multi_processor_count + 2)
+    ref = fem2d.make_problem(spec)
+    lv = ref.levels[0]
+    rng = np.random.default_rng(5)
+    U = rng.standard_normal((B, n)) * 1e-3
+    dt0 = 0.02 / 2 ** 16
+    mult = 1 + rng.integers(0, 2, B)
+    tn = np.sort(rng.uniform(0.001, 0.02, B))
+    tp = tn - dt0 * mult
+    dev = prob.device
+    out = torch.empty(B, n, dtype=torch.float64, device=dev)
+    prob.phi_batch(0, torch.as_tensor(U, device=dev), torch.as_tensor(1.0 / (tn - tp), device=dev),
+                   torch.as_tensor(prob.source_values(tn), device=dev), out)
+    got = out.cpu().numpy()
+    dts = tn - tp
+    F = np.stack([ref.forcing(float(t)) for t in tn])
+    exp = np.empty_like(U)
+    for dt in np.unique(dts):
+        idx = np.nonzero(dts == dt)[0]
+        lu = spla.splu((lv.K + lv.M * (1.0 / dt)).tocsc())
+        rhs = F[idx] + (1.0 / dt) * (lv.M @ U[idx].T).T
+        exp[idx] = lu.solve(rhs.T).T
+    err = np.linalg.norm(got - exp, axis=1) / np.linalg.norm(exp, axis=1)
+    assert err.max() < 1e-11, err.max()

@@ -6,10 +6,15 @@ import torch
 sys.path.insert(0, '.')
 from paper_1912_03106_b200 import GpuFemProblem, configs, build
 build.build()
-spec = configs.config2(N=128, n_steps=2 ** 14, levels=3, grids=2, strategy="delayed")
+if len(sys.argv) > 1 and sys.argv[1] == "cfg4":
+    spec = configs.config4()
+    shapes = [(0, 4096), (0, 1024), (0, 1), (1, 256), (1, 1)]
+else:
+    spec = configs.config2(N=128, n_steps=2 ** 14, levels=3, grids=2, strategy="delayed")
+    shapes = [(0, 1024), (0, 64), (0, 1), (1, 64), (1, 1)]
 prob = GpuFemProblem(spec, inner="cholesky")
 dev = prob.device
-for level, B in [(0, 1024), (0, 64), (0, 1), (1, 64), (1, 1)]:
+for level, B in shapes:
     n = prob.spatial.size(level)
     U = torch.as_tensor(np.random.default_rng(0).standard_normal((B, n)) * 1e-3, device=dev)
     dt = 0.02 / 2 ** 14
@@ -18,7 +23,7 @@ for level, B in [(0, 1024), (0, 64), (0, 1), (1, 64), (1, 1)]:
     out = torch.empty_like(U)
     prob.phi_batch(level, U, inv, src, out)        # factor
     torch.cuda.synchronize()
-    reps = 20
+    reps = 20 if B * n < 1e8 else 3
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record()

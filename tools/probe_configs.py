@@ -21,6 +21,10 @@ elif name == "cfg3":
     spec = configs.config3(grids=2, strategy="delayed")
 elif name == "cfg3-window":
     spec = configs.config3(n_steps=2 ** 10, grids=2, strategy="delayed")
+elif name in ("cfg4", "cfg4-window"):
+    spec = configs.config4(n_steps=2 ** 12 if name == "cfg4-window" else 2 ** 16)
+    if name == "cfg4-window":
+        spec["tf"] = spec["tf"] * 2 ** 12 / 2 ** 16
 else:
     raise SystemExit(name)
 prob = GpuFemProblem(spec)
