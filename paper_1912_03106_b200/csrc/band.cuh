@@ -370,13 +370,14 @@ k_band_chain(BandSolveArgs a) {
 // sequential stepper, sparse coarse levels): 128 threads = 32 rows x 4 lanes,
 // each lane a quarter of the K = 32 + W dot product with plain fp64 FMAs in
 // two accumulators, reduced by two shuffles; one barrier per block step.
-// smem (doubles): stage[2][NB * LDA], ring[2 NSLOT][NB], sb[2][NB]
-template <int CW, int NCHK, bool FWD>
+// NS-deep TMA ring (the one-column chain is latency-bound: keep NS - 1
+// blocks in flight).  smem (doubles): stage[NS][block], ring[2 NSLOT][NB], sb[2][NB]
+template <int CW, int NCHK, int NS, bool FWD>
 __global__ void __launch_bounds__(BD_CT)
 k_band_chain1(BandSolveArgs a) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ __align__(8) uint64_t bar[BD_NST];
-    constexpr int NST = BD_NST;
+    __shared__ __align__(8) uint64_t bar[NS];
+    constexpr int NST = NS;
     constexpr int NSLOT = CW * NCHK / BD_NB;
     constexpr int BLK = BD_NB * (BD_PD + NCHK * (CW + 4));
     const int4 ch = a.chunks[blockIdx.x];
@@ -411,12 +412,12 @@ k_band_chain1(BandSolveArgs a) {
     }
     for (int s = 0; s < a.nblk; ++s) {
         const int k = blk_of(s);
-        const int st = s & 1;
+        const int st = s % NST;
         const int sb_cur = s & 1;
         // keep nst - 1 blocks in flight: issue block s + nst - 1 into the stage
         // freed by block s - 1 (all threads passed the previous barrier)
         if (threadIdx.x == 0 && s + NST - 1 < a.nblk) {
-            const int sn = (s + 1) & 1;
+            const int sn = (s + NST - 1) % NST;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[sn], blk_bytes);
             tma_load_1d(stage + (size_t)sn * BLK,
@@ -426,29 +427,27 @@ k_band_chain1(BandSolveArgs a) {
             sb[(sb_cur ^ 1) * NB + threadIdx.x] = breg;
             if (s + 2 < a.nblk) breg = Ycol[NB * blk_of(s + 2) + threadIdx.x];
         }
-        mbar_wait(&bar[st], (s >> 1) & 1);
+        mbar_wait(&bar[st], (s / NST) & 1);
         const double* Lst = stage + (size_t)st * BLK;
         const double* Lrow = Lst + r * BD_PD;
         const double* bb = sb + sb_cur * NB;
-        double a0 = 0.0, a1 = 0.0;
+        // 8 independent accumulators: the fp64 FMA latency, not the issue
+        // rate, bounds a 4-lane row dot product
+        double acc[8];
 #pragma unroll
-        for (int j = sub; j < NB; j += 8) {
-            a0 = fma(Lrow[j], bb[j], a0);
-            a1 = fma(Lrow[j + 4], bb[j + 4], a1);
-        }
+        for (int t = 0; t < 8; ++t) acc[t] = Lrow[sub + 4 * t] * bb[sub + 4 * t];
+        const double* Lw = Lst + NB * BD_PD + r * (CW + 4) + sub;
 #pragma unroll
-        for (int j = sub; j < W; j += 8) {
-            const int jb0 = j / NB, jb1 = (j + 4) / NB;
-            const int b0 = FWD ? (k - NSLOT + jb0) : (k + 1 + jb0);
-            const int b1 = FWD ? (k - NSLOT + jb1) : (k + 1 + jb1);
-            const bool ok0 = FWD ? (b0 >= 0) : (b0 < a.nblk);
-            const bool ok1 = FWD ? (b1 >= 0) : (b1 < a.nblk);
-            const double w0 = ok0 ? ring[(b0 & RMASK) * NB + (j % NB)] : 0.0;
-            const double w1 = ok1 ? ring[(b1 & RMASK) * NB + ((j + 4) % NB)] : 0.0;
-            const double* Lw = Lst + NB * BD_PD + r * (CW + 4);
-            a0 = fma(-Lw[(j / CW) * NB * (CW + 4) + j % CW], w0, a0);
-            a1 = fma(-Lw[((j + 4) / CW) * NB * (CW + 4) + (j + 4) % CW], w1, a1);
+        for (int t = 0; t < W / 4; ++t) {
+            const int wb = t / 8;                     // window block (compile time)
+            const int blk = FWD ? (k - NSLOT + wb) : (k + 1 + wb);
+            const bool ok = FWD ? (blk >= 0) : (blk < a.nblk);
+            const double w = ok ? ring[(blk & RMASK) * NB + sub + 4 * (t % 8)] : 0.0;
+            const int j = 4 * t;                      // + sub
+            acc[t % 8] = fma(-Lw[(j / CW) * NB * (CW + 4) + j % CW], w, acc[t % 8]);
         }
+        const double a0 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        const double a1 = (acc[4] + acc[5]) + (acc[6] + acc[7]);
         double v = a0 + a1;
         v += __shfl_xor_sync(0xffffffffu, v, 1);
         v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -474,12 +473,18 @@ k_band_chain1(BandSolveArgs a) {
 // staged in smem one step ahead; one named barrier (128 consumer threads)
 // per block step.
 #define BD_PCT 160
-#define BD_NBUF 4
+#define BD_NBUF_MAX 6
+__host__ __device__ constexpr int bd_nbuf(int BC) { return BC == 1 ? 6 : 4; }
+// one-column chain: TMA ring depth by window
+// (measured round 1: 2 -- a 4-deep ring is 13% slower at W = 128, and a
+// register-direct LDG variant without TMA 60% slower)
+__host__ __device__ constexpr int bd_ns1(int W) { return W > 0 ? 2 : 2; }
 template <int BC, int CW, int NCHK, bool FWD>
 __global__ void __launch_bounds__(BD_PCT)
 k_band_pipe(BandSolveArgs a) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ __align__(8) uint64_t full[BD_NBUF], empty[BD_NBUF];
+    __shared__ __align__(8) uint64_t full[BD_NBUF_MAX], empty[BD_NBUF_MAX];
+    constexpr int BD_NBUF = bd_nbuf(BC);
     const int4 ch = a.chunks[blockIdx.x];
     const double* F = a.F[ch.x];
     const int col0 = ch.y, ncol = ch.z;
@@ -570,8 +575,11 @@ k_band_pipe(BandSolveArgs a) {
         for (int c = 0; c < NACC; ++c)
 #pragma unroll
             for (int nt = 0; nt < NT8; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
-        double f0 = 0.0, f1 = 0.0;                      // BC == 1 accumulators
+        double f[8];                                    // BC == 1 accumulators
+#pragma unroll
+        for (int t = 0; t < 8; ++t) f[t] = 0.0;
         const double* bb = sb + (size_t)sbc * NB * RS;
+#pragma unroll
         for (int j = 0; j < NPB; ++j) {
             const int P = s * NPB + j;
             const int buf = P % BD_NBUF;
@@ -580,12 +588,9 @@ k_band_pipe(BandSolveArgs a) {
             if (j == 0) {
                 // D^-1 b_k  (piece 0, row stride BD_PD)
                 if (BC == 1) {
-                    const double* Lr = pc + r1 * BD_PD;
+                    const double* Lr = pc + r1 * BD_PD + sub;
 #pragma unroll
-                    for (int q = sub; q < NB; q += 8) {
-                        f0 = fma(Lr[q], bb[q], f0);
-                        f1 = fma(Lr[q + 4], bb[q + 4], f1);
-                    }
+                    for (int t = 0; t < 8; ++t) f[t] = fma(Lr[4 * t], bb[sub + 4 * t], f[t]);
                 } else {
                     const double* Lr = pc + lrow * BD_PD;
 #pragma unroll
@@ -601,19 +606,15 @@ k_band_pipe(BandSolveArgs a) {
             } else {
                 const int jc = j - 1;                   // window chunk
                 if (BC == 1) {
-                    const double* Lr = pc + r1 * (CW + 4);
-#pragma unroll 4
-                    for (int q = sub; q < CW; q += 8) {
-                        const int jg0 = jc * CW + q, jg1 = jg0 + 4;
-                        const int wb0 = jg0 / NB, wb1 = jg1 / NB;
-                        const bool ok0 = FWD ? (blk0 + wb0 >= 0) : (blk0 + wb0 < a.nblk);
-                        const bool ok1 = FWD ? (blk0 + wb1 >= 0) : (blk0 + wb1 < a.nblk);
-                        int sl0 = slot0 + wb0; if (sl0 >= NR) sl0 -= NR;
-                        int sl1 = slot0 + wb1; if (sl1 >= NR) sl1 -= NR;
-                        const double w0 = ok0 ? ring[sl0 * NB + (jg0 % NB)] : 0.0;
-                        const double w1 = ok1 ? ring[sl1 * NB + (jg1 % NB)] : 0.0;
-                        f0 = fma(-Lr[q], w0, f0);
-                        f1 = fma(-Lr[q + 4], w1, f1);
+                    const double* Lr = pc + r1 * (CW + 4) + sub;
+#pragma unroll
+                    for (int t = 0; t < CW / 4; ++t) {
+                        const int jg = jc * CW + 4 * t;     // window row - sub
+                        const int wb = jg / NB;
+                        const bool ok = FWD ? (blk0 + wb >= 0) : (blk0 + wb < a.nblk);
+                        int sl = slot0 + wb; if (sl >= NR) sl -= NR;
+                        const double w = ok ? ring[sl * NB + (jg % NB) + sub] : 0.0;
+                        f[t % 8] = fma(-Lr[4 * t], w, f[t % 8]);
                     }
                 } else {
                     const double* Lr = pc + lrow * (CW + 4);
@@ -640,7 +641,7 @@ k_band_pipe(BandSolveArgs a) {
         // combine, store into the ring slot of block k and to global
         double* slotp = ring + (size_t)(k % NR) * NB * RS;
         if (BC == 1) {
-            double v = f0 + f1;
+            double v = ((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7]));
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
             if (sub == 0) {
@@ -667,30 +668,68 @@ k_band_pipe(BandSolveArgs a) {
 
 // Y[gc] = c M u_prev + f  (CSR), or Y[gc] = copy_src[perm[gc]] when
 // copy_src is given (preconditioner applications); padded rows zero
-__global__ void k_band_rhs(int n, int ldy, const int* __restrict__ row_ptr,
-                           const int* __restrict__ col_idx, const double* __restrict__ m_val,
-                           int n_src, const double* __restrict__ shapes,
-                           const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
-                           const double* __restrict__ src, const int* __restrict__ perm,
-                           double* __restrict__ Y, const double* __restrict__ copy_src) {
-    const int gc = blockIdx.y;
-    const int b = perm[gc];
-    double* y = Y + (size_t)gc * ldy;
-    if (copy_src) {
-        const double* x = copy_src + (size_t)b * n;
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ldy; i += gridDim.x * blockDim.x)
-            y[i] = i < n ? x[i] : 0.0;
-        return;
+#define BD_RHS_CB 8
+#define BD_RHS_NS 4
+__global__ void __launch_bounds__(256)
+k_band_rhs(int n, int ldy, int B, const int* __restrict__ row_ptr,
+           const int* __restrict__ col_idx, const double* __restrict__ m_val, int n_src,
+           const double* __restrict__ shapes, const double* __restrict__ u_prev,
+           const double* __restrict__ inv_dt, const double* __restrict__ src,
+           const int* __restrict__ perm, double* __restrict__ Y,
+           const double* __restrict__ copy_src) {
+    // thread = one row of BD_RHS_CB grouped columns: the row's CSR entries
+    // and source shapes are read once, the column gathers are independent
+    const int gc0 = blockIdx.y * BD_RHS_CB;
+    const int ncol = min(BD_RHS_CB, B - gc0);
+    const double* ub[BD_RHS_CB];
+    double cb[BD_RHS_CB], sv[BD_RHS_CB][BD_RHS_NS];
+    double* yb[BD_RHS_CB];
+    const double* base = copy_src ? copy_src : u_prev;
+    const int ns = n_src <= BD_RHS_NS ? n_src : 0;
+#pragma unroll
+    for (int j = 0; j < BD_RHS_CB; ++j) {
+        const int b = perm[gc0 + min(j, ncol - 1)];
+        ub[j] = base + (size_t)b * n;
+        yb[j] = Y + (size_t)(gc0 + min(j, ncol - 1)) * ldy;
+        cb[j] = copy_src ? 0.0 : inv_dt[b];
+#pragma unroll
+        for (int s = 0; s < BD_RHS_NS; ++s)
+            sv[j][s] = (!copy_src && s < ns) ? src[b * n_src + s] : 0.0;
     }
-    const double c = inv_dt[b];
-    const double* u = u_prev + (size_t)b * n;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ldy; i += gridDim.x * blockDim.x) {
-        if (i >= n) { y[i] = 0.0; continue; }
-        double mu = 0.0;
-        for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) mu = fma(m_val[e], u[col_idx[e]], mu);
-        double f = 0.0;
-        for (int s = 0; s < n_src; ++s) f = fma(src[b * n_src + s], shapes[(size_t)s * n + i], f);
-        y[i] = fma(c, mu, f);
+        double acc[BD_RHS_CB];
+        if (i >= n) {
+#pragma unroll
+            for (int j = 0; j < BD_RHS_CB; ++j) acc[j] = 0.0;
+        } else if (copy_src) {
+#pragma unroll
+            for (int j = 0; j < BD_RHS_CB; ++j) acc[j] = ub[j][i];
+        } else {
+#pragma unroll
+            for (int j = 0; j < BD_RHS_CB; ++j) acc[j] = 0.0;
+            const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
+            for (int e = e0; e < e1; ++e) {
+                const int cidx = col_idx[e];
+                const double mv = m_val[e];
+#pragma unroll
+                for (int j = 0; j < BD_RHS_CB; ++j) acc[j] = fma(mv, ub[j][cidx], acc[j]);
+            }
+            double sh[BD_RHS_NS];
+#pragma unroll
+            for (int s = 0; s < BD_RHS_NS; ++s) sh[s] = s < ns ? shapes[(size_t)s * n + i] : 0.0;
+#pragma unroll
+            for (int j = 0; j < BD_RHS_CB; ++j) {
+                double f = 0.0;
+#pragma unroll
+                for (int s = 0; s < BD_RHS_NS; ++s) f = fma(sv[j][s], sh[s], f);
+                for (int s = ns; s < n_src; ++s)       // > BD_RHS_NS sources: generic
+                    f = fma(src[(size_t)(ub[j] - base) / n * n_src + s], shapes[(size_t)s * n + i], f);
+                acc[j] = fma(cb[j], acc[j], f);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < BD_RHS_CB; ++j)
+            if (j < ncol) yb[j][i] = acc[j];
     }
 }
 

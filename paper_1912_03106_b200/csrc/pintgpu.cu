@@ -763,13 +763,13 @@ static int band_solve_bc(const Level& L, int B, int n_sm) {
 // window ring + double-buffered b
 static size_t band_solve_smem(const Level& L, int BC) {
     const int rs = BC == 1 ? 1 : BC + 4;
-    if (L.bwin <= 256)          // whole-block TMA, 2 stages, 2 NSLOT ring
-        return (BD_NST * bd_block_doubles(L.bwin) + (size_t)2 * (L.bwin / BD_NB) * BD_NB * rs +
+    if (L.bwin <= 256)          // whole-block TMA ring, 2 NSLOT window ring
+        return ((BC == 1 ? bd_ns1(L.bwin) : BD_NST) * bd_block_doubles(L.bwin) + (size_t)2 * (L.bwin / BD_NB) * BD_NB * rs +
                 2 * (size_t)BD_NB * rs) * sizeof(double);
     // pipelined: BD_NBUF operand pieces + (NSLOT+1)-slot ring + 2 b buffers
     const int cw = bd_cw(L.bwin);
     const size_t piece = (size_t)BD_NB * std::max(cw + 4, BD_PD);
-    return (BD_NBUF * piece + (size_t)(L.bwin / BD_NB + 1) * BD_NB * rs +
+    return (bd_nbuf(BC) * piece + (size_t)(L.bwin / BD_NB + 1) * BD_NB * rs +
             2 * (size_t)BD_NB * rs) * sizeof(double);
 }
 
@@ -849,8 +849,9 @@ static int launch_band(pg_ctx* ctx, BandSolveArgs sa, double** d_FU, int nch, si
         return launch_pair(ctx, k_band_pipe<BC, CW, NCHK, true>, k_band_pipe<BC, CW, NCHK, false>,
                            BD_PCT, sa, d_FU, nch, sm, st);
     else if constexpr (BC == 1)
-        return launch_pair(ctx, k_band_chain1<CW, NCHK, true>, k_band_chain1<CW, NCHK, false>,
-                           BD_CT, sa, d_FU, nch, sm, st);
+        return launch_pair(ctx, k_band_chain1<CW, NCHK, bd_ns1(CW * NCHK), true>,
+                           k_band_chain1<CW, NCHK, bd_ns1(CW * NCHK), false>, BD_CT, sa, d_FU,
+                           nch, sm, st);
     else
         return launch_pair(ctx, k_band_chain<BC, CW, NCHK, true>,
                            k_band_chain<BC, CW, NCHK, false>, BD_CT, sa, d_FU, nch, sm, st);
@@ -975,9 +976,9 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         L.Y_B = B;
         CU(cudaMalloc(&L.Y, (size_t)B * L.np * sizeof(double)));
     }
-    dim3 gr(std::max(1, std::min(32, (L.np + 255) / 256)), B);
-    k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, L.row_ptr, L.col_idx, L.m_val, L.n_src, L.shapes,
-                                   u_prev, inv_dt, src, d_perm, L.Y, copy_src);
+    dim3 gr((L.np + 255) / 256, (B + BD_RHS_CB - 1) / BD_RHS_CB);
+    k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, B, L.row_ptr, L.col_idx, L.m_val, L.n_src,
+                                   L.shapes, u_prev, inv_dt, src, d_perm, L.Y, copy_src);
     LAUNCHED();
     BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL};
     const size_t sm = band_solve_smem(L, BC);

@@ -12,6 +12,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "cfg4":
 else:
     spec = configs.config2(N=128, n_steps=2 ** 14, levels=3, grids=2, strategy="delayed")
     shapes = [(0, 1024), (0, 64), (0, 1), (1, 64), (1, 1)]
+if len(sys.argv) > 2:                      # only these "level:B" shapes
+    shapes = [tuple(int(x) for x in a.split(":")) for a in sys.argv[2:]]
 prob = GpuFemProblem(spec, inner="cholesky")
 dev = prob.device
 for level, B in shapes:
