@@ -225,6 +225,12 @@ struct BandSolveArgs {
     double* Y;                   // [n_cols][ldy] grouped columns, in place
     const int4* chunks;          // (factor, first grouped column, count, 0)
     double* const* F;            // per factor: FL or FU base (chain operands)
+    // SPIKE partition of the block chain (latency-bound batches): blockIdx.y
+    // = chunk p0 + y of P, blocks [p q, (p + 1) q) (the last chunk to nblk);
+    // q >= nblk, P = 1 is the plain sequential chain.  spike != 0: b = 0 and
+    // the window before (FWD) / after (BWD) the chunk starts as unit vectors
+    // (column c of the chunk group = window index col0 + c).
+    int q, P, p0, spike;
 };
 
 // The sequential chain:  y_k = D_k^-1 b_k - (D_k^-1 L_win) y_window
@@ -263,19 +269,33 @@ k_band_chain(BandSolveArgs a) {
     constexpr int BPT = BC / 4;
     const int brow = threadIdx.x & 31, bcol = threadIdx.x >> 5;
 
-    for (int t = threadIdx.x; t < 2 * NSLOT * NB * RS; t += BD_CT) ring[t] = 0.0;
     if (threadIdx.x == 0) {
         for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
         mbar_fence_init();
     }
-    auto blk_of = [&](int s) { return FWD ? s : a.nblk - 1 - s; };
+    const int pch = a.p0 + blockIdx.y;
+    const int s0 = pch * a.q;
+    const int s1 = pch + 1 == a.P ? a.nblk : s0 + a.q;
+    const int nsteps = s1 - s0;
+    const int lo = s0 - (a.spike ? NSLOT : 0), hi = s1 + (a.spike ? NSLOT : 0);
+    auto blk_of = [&](int s) { return FWD ? s0 + s : s1 - 1 - s; };
+    // window ring: zero, or (spike) unit vectors in the blocks before / after
+    for (int t = threadIdx.x; t < 2 * NSLOT * NB * RS; t += BD_CT) {
+        double v = 0.0;
+        if (a.spike) {
+            const int slot = t / (NB * RS), rr = (t / RS) % NB, c = t % RS;
+            const int wb = (slot - (FWD ? s0 - NSLOT : s1)) & RMASK;
+            v = (wb < NSLOT && c < ncol && wb * NB + rr == col0 + c) ? 1.0 : 0.0;
+        }
+        ring[t] = v;
+    }
     double breg[BPT];
     auto load_b = [&](int s) {
         const int rr = NB * blk_of(s) + brow;
 #pragma unroll
         for (int j = 0; j < BPT; ++j) {
             const int cc = bcol + 4 * j;
-            breg[j] = cc < ncol ? a.Y[(size_t)(col0 + cc) * a.ldy + rr] : 0.0;
+            breg[j] = (!a.spike && cc < ncol) ? a.Y[(size_t)(col0 + cc) * a.ldy + rr] : 0.0;
         }
     };
     auto store_b = [&](int buf) {
@@ -284,22 +304,22 @@ k_band_chain(BandSolveArgs a) {
     };
     load_b(0);
     store_b(0);
-    if (a.nblk > 1) load_b(1);
+    if (nsteps > 1) load_b(1);
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int q = 0; q + 1 < NST && q < a.nblk; ++q) {
+        for (int q = 0; q + 1 < NST && q < nsteps; ++q) {
             mbar_arrive_expect_tx(&bar[q], blk_bytes);
             tma_load_1d(stage + (size_t)q * BLK, F + (size_t)blk_of(q) * BLK,
                         blk_bytes, &bar[q]);
         }
     }
-    for (int s = 0; s < a.nblk; ++s) {
+    for (int s = 0; s < nsteps; ++s) {
         const int k = blk_of(s);
         const int st = s & 1;
         const int sb_cur = s & 1;
         // keep nst - 1 blocks in flight: issue block s + nst - 1 into the stage
         // freed by block s - 1 (all threads passed the previous barrier)
-        if (threadIdx.x == 0 && s + NST - 1 < a.nblk) {
+        if (threadIdx.x == 0 && s + NST - 1 < nsteps) {
             const int sn = (s + 1) & 1;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[sn], blk_bytes);
@@ -307,9 +327,9 @@ k_band_chain(BandSolveArgs a) {
                         F + (size_t)blk_of(s + NST - 1) * BLK, blk_bytes, &bar[sn]);
         }
         // b of block s+1 (in registers since the previous step) -> smem; prefetch s+2
-        if (s + 1 < a.nblk) {
+        if (s + 1 < nsteps) {
             store_b(sb_cur ^ 1);
-            if (s + 2 < a.nblk) load_b(s + 2);
+            if (s + 2 < nsteps) load_b(s + 2);
         }
         double acc[NCH][NT8][2], dacc[2][NT8][2];
 #pragma unroll
@@ -339,7 +359,7 @@ k_band_chain(BandSolveArgs a) {
         for (int j = 0; j < W; j += 4) {
             const int wbi = j / NB;
             const int blk = FWD ? (k - NSLOT + wbi) : (k + 1 + wbi);
-            const bool ok = FWD ? (blk >= 0) : (blk < a.nblk);
+            const bool ok = FWD ? (blk >= lo) : (blk < hi);
             const int slot = blk & RMASK;
             const double av = -Lst[NB * BD_PD + (j / CW) * NB * (CW + 4) + lrow * (CW + 4) +
                                    (j % CW) + q4];
@@ -398,34 +418,39 @@ k_band_chain1(BandSolveArgs a) {
         for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
         mbar_fence_init();
     }
-    auto blk_of = [&](int s) { return FWD ? s : a.nblk - 1 - s; };
+    const int pch = a.p0 + blockIdx.y;
+    const int s0 = pch * a.q;
+    const int s1 = pch + 1 == a.P ? a.nblk : s0 + a.q;
+    const int nsteps = s1 - s0;
+    const int lo = s0 - (a.spike ? NSLOT : 0), hi = s1 + (a.spike ? NSLOT : 0);
+    auto blk_of = [&](int s) { return FWD ? s0 + s : s1 - 1 - s; };
     double breg = 0.0;
     if (threadIdx.x < NB) sb[threadIdx.x] = Ycol[NB * blk_of(0) + threadIdx.x];
-    if (threadIdx.x < NB && a.nblk > 1) breg = Ycol[NB * blk_of(1) + threadIdx.x];
+    if (threadIdx.x < NB && nsteps > 1) breg = Ycol[NB * blk_of(1) + threadIdx.x];
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int q = 0; q + 1 < NST && q < a.nblk; ++q) {
+        for (int q = 0; q + 1 < NST && q < nsteps; ++q) {
             mbar_arrive_expect_tx(&bar[q], blk_bytes);
             tma_load_1d(stage + (size_t)q * BLK, F + (size_t)blk_of(q) * BLK,
                         blk_bytes, &bar[q]);
         }
     }
-    for (int s = 0; s < a.nblk; ++s) {
+    for (int s = 0; s < nsteps; ++s) {
         const int k = blk_of(s);
         const int st = s % NST;
         const int sb_cur = s & 1;
         // keep nst - 1 blocks in flight: issue block s + nst - 1 into the stage
         // freed by block s - 1 (all threads passed the previous barrier)
-        if (threadIdx.x == 0 && s + NST - 1 < a.nblk) {
+        if (threadIdx.x == 0 && s + NST - 1 < nsteps) {
             const int sn = (s + NST - 1) % NST;
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[sn], blk_bytes);
             tma_load_1d(stage + (size_t)sn * BLK,
                         F + (size_t)blk_of(s + NST - 1) * BLK, blk_bytes, &bar[sn]);
         }
-        if (threadIdx.x < NB && s + 1 < a.nblk) {
+        if (threadIdx.x < NB && s + 1 < nsteps) {
             sb[(sb_cur ^ 1) * NB + threadIdx.x] = breg;
-            if (s + 2 < a.nblk) breg = Ycol[NB * blk_of(s + 2) + threadIdx.x];
+            if (s + 2 < nsteps) breg = Ycol[NB * blk_of(s + 2) + threadIdx.x];
         }
         mbar_wait(&bar[st], (s / NST) & 1);
         const double* Lst = stage + (size_t)st * BLK;
@@ -441,7 +466,7 @@ k_band_chain1(BandSolveArgs a) {
         for (int t = 0; t < W / 4; ++t) {
             const int wb = t / 8;                     // window block (compile time)
             const int blk = FWD ? (k - NSLOT + wb) : (k + 1 + wb);
-            const bool ok = FWD ? (blk >= 0) : (blk < a.nblk);
+            const bool ok = FWD ? (blk >= lo) : (blk < hi);
             const double w = ok ? ring[(blk & RMASK) * NB + sub + 4 * (t % 8)] : 0.0;
             const int j = 4 * t;                      // + sub
             acc[t % 8] = fma(-Lw[(j / CW) * NB * (CW + 4) + j % CW], w, acc[t % 8]);
@@ -457,6 +482,147 @@ k_band_chain1(BandSolveArgs a) {
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------
+// SPIKE recombination.  Chunk p of the partitioned chain produced z_p with a
+// zero window; the true solution is y_p = z_p + G_p t, t = the true values
+// of the W rows bordering the chunk (the tail of chunk p - 1 forward, the
+// head of chunk p + 1 backward) and G_p = the chunk's response to unit
+// window values (computed once per factor with spike = 1).  Only the border
+// rows need the sequential pass over the chunks; everything else is a
+// parallel rank-W update.
+struct SpikeArgs {
+    int W, q, P, nblk, ldy, ldt;
+    double* Y;                   // [cols][ldy]
+    const int4* chunks;          // column groups (factor, first column, count)
+    double* const* G;            // per factor: [W][ldy]
+    double* T;                   // [P][ldt][W] border values per chunk
+};
+
+__device__ __forceinline__ int spike_s0(const SpikeArgs& a, int p) { return p * a.q; }
+__device__ __forceinline__ int spike_s1(const SpikeArgs& a, int p) {
+    return p + 1 == a.P ? a.nblk : (p + 1) * a.q;
+}
+
+// sequential border pass: one 1024-thread CTA per column group; thread
+// (row i, slice sl) owns W / S terms of the row's W-term dot product, the
+// S partials are reduced by all threads (output (c, i) per thread), so every
+// border step is one round of independent loads, FMAs and two barriers.
+// smem: tv[BCM][W] border values, red[S][BCM][W] partials.  T: [P][ldt][W].
+template <int BCM, int W, bool FWD>
+__global__ void __launch_bounds__(1024)
+k_spike_border(SpikeArgs a) {
+    constexpr int S = 1024 / W, JP = W / S, NO = W * BCM;
+    extern __shared__ __align__(16) double sh[];
+    double* tv = sh;
+    double* red = sh + NO;
+    const int4 ch = a.chunks[blockIdx.x];
+    const double* G = a.G[ch.x];
+    const int col0 = ch.y, ncol = ch.z;
+    const int i = threadIdx.x % W, sl = threadIdx.x / W;
+    auto border = [&](int p) {                          // first row of the border of chunk p
+        return FWD ? spike_s1(a, p) * BD_NB - W : spike_s0(a, p) * BD_NB;
+    };
+    auto zval = [&](int p, int t) {                     // z of output t = (c, row)
+        const int c = t / W, r = border(p) + t % W;
+        return c < ncol ? a.Y[(size_t)(col0 + c) * a.ldy + r] : 0.0;
+    };
+    auto tout = [&](int p, int t, double v) {
+        const int c = t / W;
+        if (c < ncol) a.T[((size_t)p * a.ldt + col0 + c) * W + t % W] = v;
+    };
+    int p = FWD ? 0 : a.P - 1;
+    for (int t = threadIdx.x; t < NO; t += 1024) {
+        const double v = zval(p, t);
+        tv[t] = v;
+        tout(p, t, v);
+    }
+    __syncthreads();
+    for (int step = 1; step + 1 < a.P; ++step) {        // the far end's border is unused
+        p = FWD ? step : a.P - 1 - step;
+        double zv[(NO + 1023) / 1024];
+#pragma unroll
+        for (int u = 0; u < (NO + 1023) / 1024; ++u) {
+            const int t = threadIdx.x + 1024 * u;
+            zv[u] = t < NO ? zval(p, t) : 0.0;
+        }
+        const int r = border(p) + i;
+        constexpr int JB = JP < 16 ? JP : 16;           // loads in flight per batch
+        double acc[BCM];
+#pragma unroll
+        for (int c = 0; c < BCM; ++c) acc[c] = 0.0;
+#pragma unroll
+        for (int j0 = 0; j0 < JP; j0 += JB) {
+            double gv[JB];
+#pragma unroll
+            for (int jj = 0; jj < JB; ++jj) gv[jj] = G[(size_t)(sl * JP + j0 + jj) * a.ldy + r];
+#pragma unroll
+            for (int c = 0; c < BCM; ++c)
+#pragma unroll
+                for (int jj = 0; jj < JB; ++jj)
+                    acc[c] = fma(gv[jj], tv[c * W + sl * JP + j0 + jj], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < BCM; ++c) red[(sl * BCM + c) * W + i] = acc[c];
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < (NO + 1023) / 1024; ++u) {
+            const int t = threadIdx.x + 1024 * u;
+            if (t < NO) {
+                double v = zv[u];
+#pragma unroll 8
+                for (int q = 0; q < S; ++q) v += red[q * NO + t];
+                tv[t] = v;
+                tout(p, t, v);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// parallel rank-W update of every non-first chunk
+// grid (row tiles of 256, P - 1 chunks, column groups)
+template <int BCM, bool FWD>
+__global__ void __launch_bounds__(256)
+k_spike_fix(SpikeArgs a) {
+    extern __shared__ __align__(16) double tv[];        // [W][BCM]
+    const int4 ch = a.chunks[blockIdx.z];
+    const double* G = a.G[ch.x];
+    const int col0 = ch.y, ncol = ch.z;
+    const int p = FWD ? 1 + blockIdx.y : blockIdx.y;    // chunk being fixed
+    const int pb = FWD ? p - 1 : p + 1;                  // chunk holding its border
+    const int r0 = spike_s0(a, p) * BD_NB, r1 = spike_s1(a, p) * BD_NB;
+    const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r0 + blockIdx.x * blockDim.x >= r1) return;      // whole tile past the chunk
+    for (int t = threadIdx.x; t < a.W * BCM; t += blockDim.x) {
+        const int c = t / a.W, j = t % a.W;
+        tv[j * BCM + c] = c < ncol ? a.T[((size_t)pb * a.ldt + col0 + c) * a.W + j] : 0.0;
+    }
+    __syncthreads();
+    if (r >= r1) return;
+    double acc[BCM];
+#pragma unroll
+    for (int c = 0; c < BCM; ++c) acc[c] = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < a.W; ++j) {
+        const double gv = G[(size_t)j * a.ldy + r];
+        if constexpr (BCM % 2 == 0) {
+            const double2* t2 = reinterpret_cast<const double2*>(tv + j * BCM);
+#pragma unroll
+            for (int c = 0; c < BCM / 2; ++c) {
+                const double2 t = t2[c];
+                acc[2 * c] = fma(gv, t.x, acc[2 * c]);
+                acc[2 * c + 1] = fma(gv, t.y, acc[2 * c + 1]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < BCM; ++c) acc[c] = fma(gv, tv[j * BCM + c], acc[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < BCM; ++c)
+        if (c < ncol) a.Y[(size_t)(col0 + c) * a.ldy + r] += acc[c];
 }
 
 // The 512-wide window (511^2 grid; 140 KB of operands per block, two

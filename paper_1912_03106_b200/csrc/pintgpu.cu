@@ -60,6 +60,14 @@ struct Level {
     struct Group { std::vector<double> key; int* perm; int4* chunks; int nch; int BC; };
     std::unordered_map<uint64_t, std::vector<Group>> groups;
     Group tmp_group{};
+    // SPIKE partition of the chains for latency-bound batches (B <= #SMs)
+    int spk_q = 0, spk_P = 1;
+    std::vector<double*> GF, GB;            // per factor: [W][np] spikes (lazy)
+    double** d_GF = nullptr;
+    double** d_GB = nullptr;
+    double* spk_T = nullptr;                // [P][W][B] border values
+    size_t spk_T_cap = 0;
+    int4* d_spk_chunks = nullptr;           // spike generation column groups
     // batched Newton-Krylov workspace
     double *nk_u = nullptr, *nk_F = nullptr, *nk_D = nullptr, *nk_rhs = nullptr,
            *nk_R = nullptr, *nk_Z = nullptr, *nk_P = nullptr, *nk_Q = nullptr,
@@ -208,13 +216,16 @@ static void free_level(Level& L) {
     void* ptrs[] = {L.row_ptr, L.col_idx, L.m_val, L.k_val, L.dM, L.dK, L.shapes,
                     L.weights, L.tile_lo, L.tile_hi, L.elem_dof, L.elem_geo,
                     L.ne_ptr, L.ne, L.mk, L.d_FL, L.d_FU, L.Y, L.d_perm,
-                    L.d_chunks, L.d_status, L.k_pre};
+                    L.d_chunks, L.d_status, L.k_pre, L.d_GF, L.d_GB, L.spk_T,
+                    L.d_spk_chunks};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : L.ws_allocs) cudaFree(p);
     L.ws_allocs.clear();
     for (double* p : L.FL) cudaFree(p);
     for (double* p : L.FU) cudaFree(p);
+    for (double* p : L.GF) if (p) cudaFree(p);
+    for (double* p : L.GB) if (p) cudaFree(p);
     for (auto& kv : L.groups)
         for (auto& gr : kv.second) { cudaFree(gr.perm); cudaFree(gr.chunks); }
     L.groups.clear();
@@ -296,6 +307,13 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
     L.nblk = (d->n + BD_NB - 1) / BD_NB;
     L.np = L.nblk * BD_NB;
     L.band_ok = L.bwin <= 512;
+    // SPIKE chunks: ~16 chunks of >= max(NSLOT, 8) blocks (windows <= 256)
+    {
+        const int nslot = L.bwin / BD_NB;
+        L.spk_q = std::max((L.nblk + 15) / 16, std::max(nslot, 8));
+        L.spk_P = L.bwin <= 256 ? L.nblk / L.spk_q : 1;
+        if (L.spk_P < 2) L.spk_P = 1;
+    }
     // rows per tile: 1024 (4 rows per thread); halo from the CSR
     L.R = 1024;
     L.n_tiles = (d->n + L.R - 1) / L.R;
@@ -787,13 +805,21 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
         L.FU.push_back(fu);
     }
     const int total = (int)L.FL.size();
+    L.GF.resize(total, nullptr);
+    L.GB.resize(total, nullptr);
     if (total > L.fac_cap) {
         if (L.d_FL) cudaFree(L.d_FL);
         if (L.d_FU) cudaFree(L.d_FU);
+        if (L.d_GF) cudaFree(L.d_GF);
+        if (L.d_GB) cudaFree(L.d_GB);
         L.fac_cap = std::max(64, 2 * total);
         CU(cudaMalloc(&L.d_FL, L.fac_cap * sizeof(double*)));
         CU(cudaMalloc(&L.d_FU, L.fac_cap * sizeof(double*)));
+        CU(cudaMalloc(&L.d_GF, L.fac_cap * sizeof(double*)));
+        CU(cudaMalloc(&L.d_GB, L.fac_cap * sizeof(double*)));
     }
+    CU(cudaMemcpyAsync(L.d_GF, L.GF.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(L.d_GB, L.GB.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(L.d_FL, L.FL.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(L.d_FU, L.FU.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
     if (!L.d_status) CU(cudaMalloc(&L.d_status, sizeof(int)));
@@ -829,41 +855,111 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     return PG_OK;
 }
 
-template <typename KF, typename KB>
-static int launch_pair(pg_ctx* ctx, KF kf, KB kb, int threads, BandSolveArgs sa, double** d_FU,
-                       int nch, size_t sm, cudaStream_t st) {
-    CU(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CU(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kf<<<nch, threads, sm, st>>>(sa);     // L y = b
-    LAUNCHED();
-    sa.F = d_FU;
-    kb<<<nch, threads, sm, st>>>(sa);     // L^T x = y
+// one triangular direction of the batched chain solve: grid (column groups, chunks)
+template <int BC, int CW, int NCHK, bool FWD>
+static int launch_dir(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, size_t sm,
+                      cudaStream_t st) {
+    if constexpr (CW * NCHK > 256) {
+        auto k = k_band_pipe<BC, CW, NCHK, FWD>;
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k<<<grid, BD_PCT, sm, st>>>(sa);
+    } else if constexpr (BC == 1) {
+        auto k = k_band_chain1<CW, NCHK, bd_ns1(CW * NCHK), FWD>;
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k<<<grid, BD_CT, sm, st>>>(sa);
+    } else {
+        auto k = k_band_chain<BC, CW, NCHK, FWD>;
+        CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k<<<grid, BD_CT, sm, st>>>(sa);
+    }
     LAUNCHED();
     return PG_OK;
 }
 
-template <int BC, int CW, int NCHK>
-static int launch_band(pg_ctx* ctx, BandSolveArgs sa, double** d_FU, int nch, size_t sm,
-                       cudaStream_t st) {
-    if constexpr (CW * NCHK > 256)
-        return launch_pair(ctx, k_band_pipe<BC, CW, NCHK, true>, k_band_pipe<BC, CW, NCHK, false>,
-                           BD_PCT, sa, d_FU, nch, sm, st);
-    else if constexpr (BC == 1)
-        return launch_pair(ctx, k_band_chain1<CW, NCHK, bd_ns1(CW * NCHK), true>,
-                           k_band_chain1<CW, NCHK, bd_ns1(CW * NCHK), false>, BD_CT, sa, d_FU,
-                           nch, sm, st);
-    else
-        return launch_pair(ctx, k_band_chain<BC, CW, NCHK, true>,
-                           k_band_chain<BC, CW, NCHK, false>, BD_CT, sa, d_FU, nch, sm, st);
+template <int CW, int NCHK>
+static int launch_dir_bc(pg_ctx* ctx, int BC, bool fwd, const BandSolveArgs& sa, dim3 grid,
+                         size_t sm, cudaStream_t st) {
+#define PG_DIR(B_)                                                                          \
+    return fwd ? launch_dir<B_, CW, NCHK, true>(ctx, sa, grid, sm, st)                    \
+               : launch_dir<B_, CW, NCHK, false>(ctx, sa, grid, sm, st);
+    if (BC == 1) { PG_DIR(1) }
+    if (BC == 8) { PG_DIR(8) }
+    if constexpr (CW * NCHK <= 256)
+        if (BC == 16) { PG_DIR(16) }
+#undef PG_DIR
+    return set_err(ctx, PG_EINVAL, "band batch width %d not supported", BC);
 }
 
-template <int CW, int NCHK>
-static int launch_band_w(pg_ctx* ctx, int BC, BandSolveArgs sa, double** d_FU, int nch,
-                         size_t sm, cudaStream_t st) {
-    if (BC == 1) return launch_band<1, CW, NCHK>(ctx, sa, d_FU, nch, sm, st);
-    if (BC == 8) return launch_band<8, CW, NCHK>(ctx, sa, d_FU, nch, sm, st);
-    if constexpr (CW * NCHK <= 256) return launch_band<16, CW, NCHK>(ctx, sa, d_FU, nch, sm, st);
-    return set_err(ctx, PG_EINVAL, "band batch width %d not supported", BC);
+static int band_dir(pg_ctx* ctx, const Level& L, int BC, bool fwd, const BandSolveArgs& sa,
+                    dim3 grid, size_t sm, cudaStream_t st) {
+    switch (L.bwin) {
+        case 32: return launch_dir_bc<32, 1>(ctx, BC, fwd, sa, grid, sm, st);
+        case 64: return launch_dir_bc<64, 1>(ctx, BC, fwd, sa, grid, sm, st);
+        case 128: return launch_dir_bc<128, 1>(ctx, BC, fwd, sa, grid, sm, st);
+        case 256: return launch_dir_bc<128, 2>(ctx, BC, fwd, sa, grid, sm, st);
+        case 512: return launch_dir_bc<128, 4>(ctx, BC, fwd, sa, grid, sm, st);
+        default: return set_err(ctx, PG_EINVAL, "band window %d not supported", L.bwin);
+    }
+}
+
+// spikes of factor f (response of every chunk's chain to unit border values),
+// computed once per factor by the 8-column chain in spike mode
+static int ensure_spikes(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
+    if (L.GF[f]) return PG_OK;
+    const size_t bytes = (size_t)L.bwin * L.np * sizeof(double);
+    CU(cudaMalloc(&L.GF[f], bytes));
+    CU(cudaMalloc(&L.GB[f], bytes));
+    CU(cudaMemsetAsync(L.GF[f], 0, bytes, st));
+    CU(cudaMemsetAsync(L.GB[f], 0, bytes, st));
+    CU(cudaMemcpyAsync(L.d_GF + f, &L.GF[f], sizeof(double*), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(L.d_GB + f, &L.GB[f], sizeof(double*), cudaMemcpyHostToDevice, st));
+    const int ng = L.bwin / 8;
+    if (!L.d_spk_chunks) CU(cudaMalloc(&L.d_spk_chunks, 64 * sizeof(int4)));   // W <= 512
+    std::vector<int4> ch(ng);
+    for (int c = 0; c < ng; ++c) ch[c] = make_int4(f, 8 * c, 8, 0);
+    CU(cudaMemcpyAsync(L.d_spk_chunks, ch.data(), ng * sizeof(int4), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));               // ch leaves scope
+    const size_t sm = band_solve_smem(L, 8);
+    BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.GF[f], L.d_spk_chunks, L.d_FL,
+                     L.spk_q, L.spk_P, 1, 1};
+    int rc;
+    if ((rc = band_dir(ctx, L, 8, true, sa, dim3(ng, L.spk_P - 1), sm, st))) return rc;
+    sa.Y = L.GB[f];
+    sa.F = L.d_FU;
+    sa.p0 = 0;
+    return band_dir(ctx, L, 8, false, sa, dim3(ng, L.spk_P - 1), sm, st);
+}
+
+template <int BCM>
+static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArgs& a, int nch,
+                           cudaStream_t st) {
+    const size_t sm = (size_t)L.bwin * BCM * sizeof(double);
+    const size_t smb = sm + (size_t)1024 * BCM * sizeof(double);   // + red[S][BCM][W]
+    switch (L.bwin) {
+#define PG_BORDER(W_)                                                                      \
+    case W_: {                                                                             \
+        auto kf = k_spike_border<BCM, W_, true>;                                           \
+        auto kb = k_spike_border<BCM, W_, false>;                                          \
+        CU(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb)); \
+        CU(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb)); \
+        if (fwd) kf<<<nch, 1024, smb, st>>>(a);                                            \
+        else kb<<<nch, 1024, smb, st>>>(a);                                                \
+        break;                                                                             \
+    }
+        PG_BORDER(32)
+        PG_BORDER(64)
+        PG_BORDER(128)
+        PG_BORDER(256)
+#undef PG_BORDER
+        default: return set_err(ctx, PG_EINVAL, "spike window %d not supported", L.bwin);
+    }
+    LAUNCHED();
+    const int rows = (L.nblk - (L.spk_P - 1) * L.spk_q) * BD_NB;     // longest (last) chunk
+    dim3 grid((rows + 255) / 256, L.spk_P - 1, nch);
+    if (fwd) k_spike_fix<BCM, true><<<grid, 256, sm, st>>>(a);
+    else k_spike_fix<BCM, false><<<grid, 256, sm, st>>>(a);
+    LAUNCHED();
+    return PG_OK;
 }
 
 static uint64_t hash_doubles(const double* v, int n) {
@@ -895,7 +991,9 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         CU(cudaMemcpyAsync(c.data(), inv_dt, B * sizeof(double), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
     }
-    const int BC = band_solve_bc(L, B, ctx->n_sm);
+    // latency-bound batches run the SPIKE-partitioned chains
+    const bool spike = L.spk_P > 1 && B <= ctx->n_sm;
+    const int BC = spike ? (B >= 16 ? 8 : 1) : band_solve_bc(L, B, ctx->n_sm);
     // cached grouping for this exact inv_dt pattern?
     const uint64_t h = hash_doubles(c.data(), B);
     Level::Group* grp = nullptr;
@@ -980,17 +1078,39 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, B, L.row_ptr, L.col_idx, L.m_val, L.n_src,
                                    L.shapes, u_prev, inv_dt, src, d_perm, L.Y, copy_src);
     LAUNCHED();
-    BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL};
+    const int P = spike ? L.spk_P : 1;
+    if (spike) {
+        std::vector<char> need(L.FL.size(), 0);
+        for (int b = 0; b < B; ++b) need[fid.empty() ? 0 : fid[b]] = 1;
+        if (fid.empty()) {                 // cached grouping: factors from the chunks
+            std::vector<int4> hch(nch);
+            CU(cudaMemcpy(hch.data(), d_chunks, nch * sizeof(int4), cudaMemcpyDeviceToHost));
+            std::fill(need.begin(), need.end(), 0);
+            for (const int4& q : hch) need[q.x] = 1;
+        }
+        for (size_t f = 0; f < need.size(); ++f)
+            if (need[f] && (rc = ensure_spikes(ctx, L, (int)f, st))) return rc;
+        const size_t tneed = (size_t)P * L.bwin * B;
+        if (tneed > L.spk_T_cap) {
+            if (L.spk_T) cudaFree(L.spk_T);
+            L.spk_T_cap = tneed;
+            CU(cudaMalloc(&L.spk_T, tneed * sizeof(double)));
+        }
+    }
+    BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL,
+                     spike ? L.spk_q : L.nblk, P, 0, 0};
     const size_t sm = band_solve_smem(L, BC);
-    sa.nst = 0;
+    SpikeArgs spa{L.bwin, L.spk_q, P, L.nblk, L.np, B, L.Y, d_chunks, L.d_GF, L.spk_T};
     if ((rc = prof_mark(ctx, 2, st))) return rc;
-    switch (L.bwin) {
-        case 32: rc = launch_band_w<32, 1>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
-        case 64: rc = launch_band_w<64, 1>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
-        case 128: rc = launch_band_w<128, 1>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
-        case 256: rc = launch_band_w<128, 2>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
-        case 512: rc = launch_band_w<128, 4>(ctx, BC, sa, L.d_FU, nch, sm, st); break;
-        default: return set_err(ctx, PG_EINVAL, "band window %d not supported", L.bwin);
+    for (int dir = 0; dir < 2 && !rc; ++dir) {
+        const bool fwd = dir == 0;
+        sa.F = fwd ? L.d_FL : L.d_FU;
+        if ((rc = band_dir(ctx, L, BC, fwd, sa, dim3(nch, P), sm, st))) break;
+        if (spike) {
+            spa.G = fwd ? L.d_GF : L.d_GB;
+            rc = BC == 1 ? spike_recombine<1>(ctx, L, fwd, spa, nch, st)
+                         : spike_recombine<8>(ctx, L, fwd, spa, nch, st);
+        }
     }
     if (rc) return rc;
     if ((rc = prof_mark(ctx, 2, st))) return rc;
