@@ -353,7 +353,91 @@ class NonlinearFemProblem(FemProblem):
         return out
 
 
+def surrogate_coupling(n_cells):
+    """Torque weights c_i = sin(2 pi x_i) h^2 of the interior nodes (x-fastest
+    numbering): the 2D form of reference problems.py:264-267."""
+    N = int(n_cells)
+    h = 1.0 / N
+    x = (np.arange(1, N) * h)[None, :] * np.ones((N - 1, 1))
+    return (np.sin(2.0 * math.pi * x) * (h * h)).reshape(-1)
+
+
+class SurrogateFemProblem:
+    """Saturating (or linear) field one-way coupled to rotor angle and speed,
+    restating reference problems.py:247-287 (SurrogateMachineProblem) on the
+    2D model: the field takes its step, then
+
+        T = c . u_new,  omega' = (omega + dt T / I) / (1 + dt friction / I),
+        theta' = theta + dt omega'.
+
+    step_batch works on augmented rows [field | theta, omega]."""
+
+    n_scalars = 2
+
+    def __init__(self, spec):
+        sg = spec["surrogate"]
+        self.inertia = float(sg.get("inertia", 1.0))
+        self.friction = float(sg.get("friction", 0.1))
+        if self.inertia <= 0.0 or self.friction < 0.0:
+            raise ValueError("need inertia > 0 and friction >= 0")
+        base = dict(spec)
+        base.pop("surrogate")
+        self.base = (NonlinearFemProblem(base) if base.get("nonlinear")
+                     else LinearFemProblem(base))
+        self.spec = spec
+        self.spatial = self.base.spatial
+        self.levels = self.base.levels
+        self.excitation = self.base.excitation
+        self.couplings = [surrogate_coupling(self.spatial.cells[g])
+                          for g in range(self.spatial.n_grids)]
+
+    def initial_state(self, spatial_level=0):
+        return BlockState.zeros(self.spatial.size(spatial_level), 2, spatial_level)
+
+    def loss_weights(self, spatial_level=0):
+        return self.base.loss_weights(spatial_level)
+
+    def source_values(self, t, smooth=False):
+        return self.base.source_values(t, smooth)
+
+    def forcing(self, t, spatial_level=0, smooth=False):
+        return self.base.forcing(t, spatial_level, smooth)
+
+    def torque(self, field, spatial_level=0):
+        return float(self.couplings[spatial_level] @ field)
+
+    def _scalars(self, theta, omega, dt, torque):
+        omega_new = ((omega + dt * torque / self.inertia)
+                     / (1.0 + dt * self.friction / self.inertia))
+        return theta + dt * omega_new, omega_new
+
+    def step(self, u_prev, t_prev, t_next, spatial_level=0, guess=None, smooth=False):
+        fp = BlockState(u_prev.field, spatial_level=spatial_level)
+        fg = (BlockState(guess.field, spatial_level=spatial_level)
+              if guess is not None else None)
+        new, diag = self.base.step(fp, t_prev, t_next, spatial_level, fg, smooth)
+        dt = t_next - t_prev
+        theta, omega = u_prev.scalars
+        th, om = self._scalars(theta, omega, dt, self.torque(new.field, spatial_level))
+        return BlockState(new.field, [th, om], spatial_level), diag
+
+    def step_batch(self, U, t_prev, t_next, spatial_level=0, smooth=False):
+        U = np.asarray(U)
+        n = self.spatial.size(spatial_level)
+        F = self.base.step_batch(np.ascontiguousarray(U[:, :n]), t_prev, t_next,
+                                 spatial_level, smooth)
+        out = np.empty_like(U)
+        out[:, :n] = F
+        dt = np.asarray(t_next) - np.asarray(t_prev)
+        for b in range(len(U)):
+            out[b, n], out[b, n + 1] = self._scalars(U[b, n], U[b, n + 1], float(dt[b]),
+                                                     self.torque(F[b], spatial_level))
+        return out
+
+
 def make_problem(spec):
+    if spec.get("surrogate"):
+        return SurrogateFemProblem(spec)
     return NonlinearFemProblem(spec) if spec.get("nonlinear") else LinearFemProblem(spec)
 
 

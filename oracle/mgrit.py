@@ -69,7 +69,11 @@ class _Level:
         self.c_idx = splitting.c_indices[1:]          # closing C-points
         self.K = len(self.c_idx)
         self.s = s_level
-        self.n = problem.spatial.size(s_level)
+        # state rows are [field | scalars] (problems with n_scalars > 0, e.g.
+        # the surrogate machine, problems.py:247-287)
+        self.nf = problem.spatial.size(s_level)
+        self.ns = int(getattr(problem, "n_scalars", 0))
+        self.n = self.nf + self.ns
         self.anchor = np.zeros(self.n)
         self.c_store = np.zeros((self.K, self.n))
         self.u_keep = np.zeros((self.n_points, self.n)) if index > 0 else None
@@ -121,14 +125,18 @@ class MgritOracle:
         return cur
 
     def _R(self, fine, coarse, X):
+        """restrict_state: field restricted, scalars copied (spatial.py:64-71)."""
         if coarse.s == fine.s:
             return X.copy()
-        return np.stack([self.problem.spatial.restrict_field(x, fine.s) for x in X])
+        return np.stack([np.concatenate([self.problem.spatial.restrict_field(x[:fine.nf], fine.s),
+                                         x[fine.nf:]]) for x in X])
 
     def _P(self, fine, coarse, X):
+        """prolong_error: field interpolated, scalars copied (spatial.py:73-84)."""
         if coarse.s == fine.s:
             return X
-        return np.stack([self.problem.spatial.prolong_field(x, coarse.s) for x in X])
+        return np.stack([np.concatenate([self.problem.spatial.prolong_field(x[:coarse.nf], coarse.s),
+                                         x[coarse.nf:]]) for x in X])
 
     # --- sweeps ---
     def _fc_sweep(self, lvl):
@@ -203,12 +211,13 @@ class MgritOracle:
         if lvl.use_rhs:
             res = res + lvl.rhs[lvl.c_idx]
         sum_sq = 0.0
-        for k in range(lvl.K):
-            sum_sq += float(res[k] @ res[k])
+        nf = lvl.nf
+        for k in range(lvl.K):                         # norm_sq, state.py:74-75
+            sum_sq += float(res[k, :nf] @ res[k, :nf]) + float(res[k, nf:] @ res[k, nf:])
         losses = np.zeros(lvl.K)
         for k, c in enumerate(lvl.c_idx):
             dt = float(lvl.t[c] - lvl.t[c - 1])
-            losses[k] = joule_loss(BlockState(last_f[k]), BlockState(lvl.c_store[k]),
+            losses[k] = joule_loss(BlockState(last_f[k, :nf]), BlockState(lvl.c_store[k, :nf]),
                                    dt, self.weights)
         return sum_sq, losses
 
@@ -276,7 +285,9 @@ class MgritOracle:
             lvl.use_rhs = False
         if initial_guess is not None:
             lvl0 = self.levels[0]
-            lvl0.c_store = np.stack([initial_guess[c].field for c in lvl0.c_idx])
+            lvl0.c_store = np.stack([np.concatenate([initial_guess[c].field,
+                                                     initial_guess[c].scalars])
+                                     for c in lvl0.c_idx])
         elif self.cycle.nested_iterations and self.n_levels > 1:
             try:
                 self._nested()

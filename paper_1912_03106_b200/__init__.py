@@ -24,7 +24,7 @@ from .excitation import Excitation
 from .mgrit import (CycleSpec, MgritSolver, SolverRun, StoppingCriterion,
                     StorageReport, mgrit_solve, qoi_change, sequential_solve,
                     storage_estimate)
-from .problem import GpuFemProblem, StepDiagnostics
+from .problem import GpuFemProblem, GpuSurrogateProblem, StepDiagnostics, make_problem
 from .runtime import Decomposition, DistTransport, NullTransport
 from .spatial import SpatialHierarchy2D, assign_spatial_levels
 from .state import BlockState, SpaceTimeVector
@@ -35,7 +35,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BlockState", "CFSplitting", "CycleSpec", "Decomposition", "DistTransport",
-    "Excitation", "GpuFemProblem", "MgritSolver", "NewtonConvergenceError",
+    "Excitation", "GpuFemProblem", "GpuSurrogateProblem", "make_problem", "MgritSolver", "NewtonConvergenceError",
     "NullTransport", "PintGpuError", "SolverRun", "SpaceTimeVector",
     "SpatialHierarchy2D", "StepDiagnostics", "StoppingCriterion", "StorageReport",
     "TimeGrid", "TimeHierarchy", "TransportError", "assign_spatial_levels",

@@ -130,5 +130,21 @@ def config5(N=256):
     return s
 
 
+def with_surrogate(spec, inertia=1.0, friction=0.1):
+    """Rotor angle / speed (theta, omega) one-way coupled to the field: the 2D
+    form of the reference's SurrogateMachineProblem (problems.py:247-287).
+    Torque = sum_i c_i u_i with c_i = sin(2 pi x_i) h^2 over the interior
+    nodes (the 2D analogue of the reference's sin(2 pi x) dx); after the field
+    step omega' = (omega + dt T / I) / (1 + dt friction / I), theta' = theta +
+    dt omega'.  The two scalars ride along every state (norms include them,
+    transfers pass them through bitwise)."""
+    if inertia <= 0.0 or friction < 0.0:
+        raise ValueError("need inertia > 0 and friction >= 0")
+    s = copy.deepcopy(spec)
+    s["surrogate"] = {"inertia": float(inertia), "friction": float(friction)}
+    s["name"] = spec.get("name", "spec") + "+surrogate"
+    return s
+
+
 CONFIGS = {"cfg1": config1, "cfg2": config2, "cfg3": config3,
            "cfg4": config4, "cfg5": config5}

@@ -142,6 +142,10 @@ class GridModel:
         self.weights = np.add.reduceat(self.m_val, self.row_ptr[:-1]) \
             if self.nnz else np.zeros(self.n)
         self._elements(spec, N, h)
+        # surrogate-machine torque weights sin(2 pi x) h^2 (configs.with_surrogate)
+        xs = np.arange(1, N) * h
+        self.coupling = np.ascontiguousarray(
+            np.tile(np.sin(2.0 * np.pi * xs) * (h * h), N - 1))
 
     def _elements(self, spec, N, h):
         """Iron elements for the matrix-free nonlinear operator."""

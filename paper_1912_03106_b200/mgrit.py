@@ -144,7 +144,9 @@ class _Level:
         self.splitting = splitting
         self.m = splitting.factor
         self.s = s_level
-        self.n = prob.spatial.size(s_level)
+        # one state row = [field | scalars] (prob.state_size)
+        self.n = prob.state_size(s_level) if hasattr(prob, "state_size") \
+            else prob.spatial.size(s_level)
         self.decomp = d = Decomposition(splitting, T.size)
         r = T.rank
         self.empty = d.is_empty(r)
@@ -618,7 +620,10 @@ class MgritSolver:
         if not lvl.K:
             return
         if hasattr(trajectory, "states"):
-            rows = torch.stack([trajectory[int(c)].field for c in lvl.c_idx])
+            rows = torch.stack([torch.cat([trajectory[int(c)].field.to(self.problem.device),
+                                           torch.as_tensor(trajectory[int(c)].scalars,
+                                                           device=self.problem.device)])
+                                for c in lvl.c_idx])
         else:
             tr = torch.as_tensor(np.asarray(trajectory) if not torch.is_tensor(trajectory)
                                  else trajectory, device=self.problem.device)
@@ -749,7 +754,8 @@ def sequential_solve(problem, times, spatial_level=0, smooth=False):
     """GPU sequential time stepping (reference problems.py:319-339): the
     time-to-solution baseline.  Returns [n, size] device trajectory."""
     n = len(times)
-    size = problem.spatial.size(spatial_level)
+    size = problem.state_size(spatial_level) if hasattr(problem, "state_size") \
+        else problem.spatial.size(spatial_level)
     dev = problem.device
     out = torch.empty(n, size, dtype=torch.float64, device=dev)
     out[0].zero_()

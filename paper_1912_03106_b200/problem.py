@@ -46,6 +46,9 @@ class GpuFemProblem:
 
     def __init__(self, spec, device=None, rtol=None, max_iters=None,
                  check_every=16, inner=None):
+        if spec.get("surrogate") and type(self) is GpuFemProblem:
+            raise ValueError("spec carries a surrogate machine: use GpuSurrogateProblem "
+                             "(or make_problem)")
         if not torch.cuda.is_available():
             raise PintGpuError("GpuFemProblem needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -137,6 +140,10 @@ class GpuFemProblem:
             pass
 
     # --- the reference contract ---------------------------------------------------
+    def state_size(self, spatial_level=0):
+        """Entries of one device state row ([field | scalars])."""
+        return self.spatial.size(spatial_level) + self.n_scalars
+
     def initial_state(self, spatial_level=0):
         return BlockState.zeros(self.spatial.size(spatial_level), 0, spatial_level,
                                 device=self.device)
@@ -253,3 +260,150 @@ class GpuFemProblem:
             self.ctx, int(coarse_level), int(bool(coarsen)), int(kept.shape[0]),
             _lib.ptr(kept), _lib.ptr(cprop), _lib.ptr(res), _lib.ptr(out),
             self.spatial.r_mode, self._stream()), "pg_fas_rhs")
+
+
+class GpuSurrogateProblem(GpuFemProblem):
+    """Rotor angle / speed one-way coupled to the field: reference
+    problems.py:247-287 (SurrogateMachineProblem) on the 2D model.  The field
+    takes the base problem's step (linear or Brauer-Newton, same kernels),
+    then per column
+
+        T = c . u_new,  omega' = (omega + dt T / I) / (1 + dt friction / I),
+        theta' = theta + dt omega',
+
+    with c = sin(2 pi x) h^2 (configs.with_surrogate).  Device states are
+    augmented rows [field | theta, omega] (state_size = n + 2): norms include
+    the scalars, transfers pass them through bitwise (spatial.py:64-84); the
+    field part runs through the C ABI on packed copies, the scalars are
+    column-wise torch ops."""
+
+    n_scalars = 2
+
+    def __init__(self, spec, **kw):
+        sg = spec.get("surrogate") or {}
+        self.inertia = float(sg.get("inertia", 1.0))
+        self.friction = float(sg.get("friction", 0.1))
+        if self.inertia <= 0.0 or self.friction < 0.0:
+            raise ValueError("need inertia > 0 and friction >= 0")
+        super().__init__(spec, **kw)
+        self._coupling = [torch.as_tensor(g.coupling, device=self.device) for g in self.grids]
+
+    def initial_state(self, spatial_level=0):
+        return BlockState.zeros(self.spatial.size(spatial_level), 2, spatial_level,
+                                device=self.device)
+
+    def torque(self, field, spatial_level=0):
+        return float(self._coupling[spatial_level] @ field.to(self.device))
+
+    def step(self, u_prev, t_prev, t_next, spatial_level=0, guess=None, smooth=False):
+        n = self.spatial.size(spatial_level)
+        if u_prev.field.numel() != n or len(u_prev.scalars) != 2:
+            raise ValueError(f"state needs {n} field entries and 2 scalars")
+        dt = float(t_next) - float(t_prev)
+        inv_dt = torch.tensor([1.0 / dt], dtype=torch.float64, device=self.device)
+        src = torch.as_tensor(self.source_values([t_next], smooth),
+                              device=self.device).reshape(1, -1)
+        row = torch.empty(1, n + 2, dtype=torch.float64, device=self.device)
+        row[0, :n] = u_prev.field.to(self.device)
+        row[0, n:] = torch.as_tensor(u_prev.scalars, device=self.device)
+        gs = None
+        if guess is not None and guess is not u_prev:
+            gs = torch.zeros_like(row)
+            gs[0, :n] = guess.field.to(self.device)
+        out = torch.empty_like(row)
+        self.phi_batch(spatial_level, row, inv_dt, src, out, guess=gs, dt_host=[dt])
+        st = self.last_stats()
+        its = st["newton_iters"] if self.nonlinear else st["batch_iters"]
+        return (BlockState(out[0, :n].clone(), out[0, n:].cpu().numpy(), spatial_level),
+                StepDiagnostics(iterations=int(its)))
+
+    def phi_batch(self, level, u_prev, inv_dt, src, out, g=None, g_idx=None, guess=None,
+                  inv_dt_host=None, dt_host=None):
+        n = self.spatial.size(level)
+        B = int(u_prev.shape[0])
+        uf = u_prev[:, :n].contiguous()
+        sc = u_prev[:, n:].clone()                     # out may alias u_prev
+        gf = guess[:, :n].contiguous() if guess is not None else None
+        of = torch.empty(B, n, dtype=torch.float64, device=self.device)
+        super().phi_batch(level, uf, inv_dt, src, of, guess=gf, inv_dt_host=inv_dt_host)
+        if dt_host is not None:
+            dt = torch.as_tensor(np.asarray(dt_host, dtype=float), device=self.device)
+        elif inv_dt_host is not None:
+            dt = torch.as_tensor(1.0 / np.asarray(inv_dt_host, dtype=float), device=self.device)
+        else:
+            dt = 1.0 / inv_dt
+        T = of @ self._coupling[level]
+        omega = (sc[:, 1] + dt * T / self.inertia) / (1.0 + dt * self.friction / self.inertia)
+        theta = sc[:, 0] + dt * omega
+        out[:, :n] = of
+        out[:, n] = theta
+        out[:, n + 1] = omega
+        if g is not None:                              # u.add_scaled(g_i), mgrit.py:372-375
+            if g_idx is None:
+                out += g[:B]
+            else:
+                sel = g_idx.long()
+                rows = (sel >= 0).nonzero().flatten()
+                if rows.numel():
+                    out[rows] += g[sel[rows]]
+
+    def restrict(self, fine_level, x, out):
+        nf, nc = self.spatial.size(fine_level), self.spatial.size(fine_level + 1)
+        of = torch.empty(x.shape[0], nc, dtype=torch.float64, device=self.device)
+        super().restrict(fine_level, x[:, :nf].contiguous(), of)
+        out[:, :nc] = of
+        out[:, nc:] = x[:, nf:]
+
+    def prolong_add(self, coarse_level, x, out, out_idx=None, beta=1.0):
+        nc, nf = self.spatial.size(coarse_level), self.spatial.size(coarse_level - 1)
+        B = int(x.shape[0])
+        tmp = torch.empty(B, nf, dtype=torch.float64, device=self.device)
+        super().prolong_add(coarse_level, x[:, :nc].contiguous(), tmp, None, 0.0)
+        rows = out_idx.long() if out_idx is not None else torch.arange(B, device=self.device)
+        if beta == 0.0:
+            out[rows, :nf] = tmp
+            out[rows, nf:] = x[:, nc:]
+        else:
+            out[rows, :nf] += tmp
+            out[rows, nf:] += x[:, nc:]
+
+    def c_residual(self, level, prop, c, sumsq, c_idx=None, g=None, g_idx=None,
+                   res=None, last_f=None, inv_dt=None, loss=None):
+        n = self.spatial.size(level)
+        B = int(prop.shape[0])
+        cs = c[c_idx.long()] if c_idx is not None else c[:B]
+        rf = torch.empty(B, n, dtype=torch.float64, device=self.device) if res is not None else None
+        super().c_residual(level, prop[:, :n].contiguous(), cs[:, :n].contiguous(), sumsq,
+                           None, g[:, :n].contiguous() if g is not None else None, g_idx,
+                           rf, last_f[:, :n].contiguous() if last_f is not None else None,
+                           inv_dt, loss)
+        rs = prop[:, n:] - cs[:, n:]
+        if g is not None:
+            if g_idx is None:
+                rs = rs + g[:B, n:]
+            else:
+                sel = g_idx.long()
+                ok = sel >= 0
+                gs = torch.zeros_like(rs)
+                gs[ok] = g[sel[ok], n:]
+                rs = torch.where(ok[:, None], rs + gs, rs)
+        sumsq[:B] += rs[:, 0] * rs[:, 0] + rs[:, 1] * rs[:, 1]   # norm_sq, state.py:74-75
+        if res is not None:
+            res[:, :n] = rf
+            res[:, n:] = rs
+
+    def fas_rhs(self, coarse_level, coarsen, kept, cprop, res, out):
+        nc = self.spatial.size(coarse_level)
+        nf = self.spatial.size(coarse_level - 1) if coarsen else nc
+        B = int(kept.shape[0])
+        of = torch.empty(B, nc, dtype=torch.float64, device=self.device)
+        super().fas_rhs(coarse_level, coarsen, kept[:, :nc].contiguous(),
+                        cprop[:, :nc].contiguous(), res[:, :nf].contiguous(), of)
+        out[:, :nc] = of
+        out[:, nc:] = (kept[:, nc:] - cprop[:, nc:]) + res[:, nf:]
+
+
+def make_problem(spec, **kw):
+    """GpuSurrogateProblem for specs with a surrogate machine, else GpuFemProblem."""
+    cls = GpuSurrogateProblem if spec.get("surrogate") else GpuFemProblem
+    return cls(spec, **kw)

@@ -62,6 +62,10 @@ def mgrit_case(name, spec, max_iters=50, tol=1e-7, with_solution=True):
         out["sol_c"] = arr[::m]
         out["sol_norms"] = np.linalg.norm(arr, axis=1)
         out["sol_final"] = arr[-1]
+        if getattr(prob, "n_scalars", 0):
+            sc = np.stack([s.scalars for s in sol.states])
+            out["sol_c_scalars"] = sc[::m]
+            out["seq_scalars"] = np.stack([s.scalars for s in seq.states])
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
     print(f"{name}: {run.iterations} iters, converged={run.converged}, "
           f"history={['%.3e' % h for h in out['history']]}  ({time.time() - t0:.1f}s)")
@@ -91,7 +95,7 @@ def phi_case(name, spec, B=8, seed=0):
 
 
 def main():
-    which = sys.argv[1:] or ["phi", "cfg1", "cfg2s", "cfg2d", "cfg3s", "variants"]
+    which = sys.argv[1:] or ["phi", "cfg1", "cfg2s", "cfg2d", "cfg3s", "variants", "surrogate"]
     if "phi" in which:
         phi_case("phi_cfg2_n32", configs.config2(N=32, n_steps=1024, levels=3))
         s = configs.config2(N=32, n_steps=1024, levels=3)
@@ -116,6 +120,12 @@ def main():
         mgrit_case("mgrit_cfg3_delayed_n32", s)
 
 
+    if "surrogate" in which:
+        # f3: rotor angle / speed coupled to the field (problems.py:247-287)
+        mgrit_case("mgrit_cfg1_surrogate", configs.with_surrogate(configs.config1()))
+        s = configs.config3(N=32, n_steps=256, levels=3, grids=2, strategy="delayed")
+        mgrit_case("mgrit_cfg3_surrogate_n32", configs.with_surrogate(s, inertia=2.0,
+                                                                      friction=0.3))
     if "variants" in which:
         # F-cycle (mgrit.py:617-626) and nested iterations (mgrit.py:659-675)
         s = configs.config2(N=32, n_steps=1024, levels=3, grids=2, strategy="delayed")

@@ -10,9 +10,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _run(spec, max_iters, tol, **kw):
-    from paper_1912_03106_b200 import (CycleSpec, GpuFemProblem, StoppingCriterion,
-                                       TimeHierarchy, build_uniform_grid, mgrit_solve)
-    prob = GpuFemProblem(spec, **kw)
+    from paper_1912_03106_b200 import (CycleSpec, StoppingCriterion, TimeHierarchy,
+                                       build_uniform_grid, make_problem, mgrit_solve)
+    prob = make_problem(spec, **kw)
     grid = build_uniform_grid(0.0, spec["tf"], spec["n_steps"])
     mg = spec["mgrit"]
     hier = TimeHierarchy.build(grid, mg["factors"])
@@ -82,3 +82,47 @@ def test_gpu_sequential_matches_reference(cuda, inner):
     assert err < 1e-9, err
     nrm = np.linalg.norm(traj, axis=1)
     assert np.allclose(nrm, fx["seq_norms"], rtol=1e-9, atol=1e-14)
+
+
+@pytest.mark.parametrize("name,hist_tol,sol_tol", [("mgrit_cfg1_surrogate", 1e-8, 1e-9),
+                                                   ("mgrit_cfg3_surrogate_n32", 1e-6, 1e-8)])
+def test_surrogate_scalars_match_reference_engine(cuda, name, hist_tol, sol_tol):
+    """f3: rotor (theta, omega) one-way coupled to the field (problems.py:247-287)
+    through the whole GPU engine: same iterations and history as the
+    reference engine, field and scalars at the C-points."""
+    fx = load_golden(name)
+    prob, grid, run, sol = _run(fx["spec"], int(fx["max_iters"]), float(fx["tol"]),
+                                inner="cholesky")
+    assert prob.n_scalars == 2
+    hist = np.array([run.initial_residual] + run.residual_norms)
+    assert run.iterations == int(fx["iterations"])
+    rel = np.abs(hist - fx["history"]) / fx["history"]
+    assert rel.max() < hist_tol, rel
+    m = int(fx["factors"][0])
+    s = sol.cpu().numpy()[::m]
+    n = fx["sol_c"].shape[1]
+    err = np.linalg.norm(s[:, :n] - fx["sol_c"]) / np.linalg.norm(fx["sol_c"])
+    assert err < sol_tol, err
+    sc = fx["sol_c_scalars"]
+    err_s = np.abs(s[:, n:] - sc).max() / np.abs(sc).max()
+    assert err_s < 1e-7, err_s
+
+
+def test_surrogate_sequential_and_step_contract(cuda):
+    fx = load_golden("mgrit_cfg1_surrogate")
+    from paper_1912_03106_b200 import (BlockState, GpuFemProblem, build_uniform_grid,
+                                       make_problem, sequential_solve)
+    prob = make_problem(fx["spec"], inner="cholesky")
+    grid = build_uniform_grid(0.0, fx["spec"]["tf"], fx["spec"]["n_steps"])
+    traj = sequential_solve(prob, grid.points).cpu().numpy()
+    n = prob.spatial.size(0)
+    ref = fx["seq_scalars"]
+    assert np.abs(traj[:, n:] - ref).max() / np.abs(ref).max() < 1e-9
+    err = np.linalg.norm(traj[-1, :n] - fx["seq_final"]) / np.linalg.norm(fx["seq_final"])
+    assert err < 1e-9, err
+    # step(): the B = 1 view with scalars in and out
+    u = BlockState(torch.as_tensor(traj[5, :n], device=prob.device), traj[5, n:])
+    out, diag = prob.step(u, float(grid.points[5]), float(grid.points[6]), 0)
+    assert np.allclose(out.scalars, traj[6, n:], rtol=1e-12, atol=0)
+    with pytest.raises(ValueError):
+        GpuFemProblem(fx["spec"])          # a surrogate spec needs the surrogate class

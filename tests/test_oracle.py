@@ -43,6 +43,42 @@ def test_oracle_engine_reproduces_reference_engine(name):
         np.testing.assert_allclose(sol[::m], fx["sol_c"], rtol=1e-12, atol=1e-18)
 
 
+def test_oracle_engine_surrogate_scalars_match_reference_engine():
+    """f3: (theta, omega) ride along every state through the reference engine
+    (reference SurrogateMachineProblem semantics, problems.py:247-287): the
+    oracle engine's augmented rows [field | theta, omega] reproduce it."""
+    fx = load_golden("mgrit_cfg1_surrogate")
+    run, sol = _oracle_run(fx)
+    hist = np.array([run.initial_residual] + run.residual_norms)
+    assert run.iterations == int(fx["iterations"])
+    np.testing.assert_allclose(hist, fx["history"], rtol=1e-12, atol=0)
+    m = int(fx["factors"][0])
+    n = fx["sol_c"].shape[1]
+    np.testing.assert_allclose(sol[::m, :n], fx["sol_c"], rtol=1e-12, atol=1e-18)
+    np.testing.assert_allclose(sol[::m, n:], fx["sol_c_scalars"], rtol=1e-10, atol=1e-22)
+
+
+def test_surrogate_step_restates_reference_update():
+    """One surrogate step by hand: field step of the base problem, torque with
+    the new field, backward-Euler speed then angle (problems.py:269-287)."""
+    from paper_1912_03106_b200 import configs
+    spec = configs.with_surrogate(configs.config1(), inertia=2.0, friction=0.5)
+    prob = fem2d.make_problem(spec)
+    base = fem2d.make_problem(configs.config1())
+    n = prob.spatial.size(0)
+    rng = np.random.default_rng(1)
+    u = fem2d.BlockState(rng.standard_normal(n) * 1e-3, [0.3, -0.7])
+    out, _ = prob.step(u, 0.001, 0.0015)
+    f, _ = base.step(fem2d.BlockState(u.field), 0.001, 0.0015)
+    assert np.array_equal(out.field, f.field)
+    dt = 0.0015 - 0.001
+    T = float(fem2d.surrogate_coupling(32) @ f.field)
+    om_ = (-0.7 + dt * T / 2.0) / (1.0 + dt * 0.5 / 2.0)
+    assert out.scalars[1] == om_ and out.scalars[0] == 0.3 + dt * om_
+    with pytest.raises(ValueError):
+        configs.with_surrogate(configs.config1(), inertia=0.0)
+
+
 def test_direct_spatial_coarsening_stalls_in_reference():
     """Documented behaviour: config 2's literal direct coarsening stalls."""
     fx = load_golden("mgrit_cfg2_direct_n32")
