@@ -17,6 +17,8 @@ OUT = os.path.join(HERE, "lib", "libpintgpu.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
          "-Xptxas", "-warn-spills"]
+# cuBLAS only for the plain rank-W GEMM of the SPIKE correction
+LIBS = ["-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 
 
 def sources():
@@ -38,7 +40,7 @@ def build(force=False, verbose=False):
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = ([nvcc] + ARCH + FLAGS + ["-I" + os.path.join(ROOT, "include"),
-                                    os.path.join(CSRC, "pintgpu.cu"), "-o", OUT])
+                                    os.path.join(CSRC, "pintgpu.cu"), "-o", OUT] + LIBS)
     if verbose:
         print(" ".join(cmd))
     r = subprocess.run(cmd, capture_output=True, text=True)

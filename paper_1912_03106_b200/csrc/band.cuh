@@ -668,7 +668,12 @@ k_band_pipe(BandSolveArgs a) {
     double* ring = bufs + (size_t)BD_NBUF * PIECE;
     double* sb = ring + (size_t)NR * NB * RS;          // [2][NB][RS]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    auto blk_of = [&](int s) { return FWD ? s : a.nblk - 1 - s; };
+    const int pch = a.p0 + blockIdx.y;                 // SPIKE chunk (BandSolveArgs)
+    const int s0 = pch * a.q;
+    const int s1 = pch + 1 == a.P ? a.nblk : s0 + a.q;
+    const int nsteps = s1 - s0;
+    const int lo = s0 - (a.spike ? NSLOT : 0), hi = s1 + (a.spike ? NSLOT : 0);
+    auto blk_of = [&](int s) { return FWD ? s0 + s : s1 - 1 - s; };
 
     if (threadIdx.x == 0) {
         for (int q = 0; q < BD_NBUF; ++q) {
@@ -677,13 +682,24 @@ k_band_pipe(BandSolveArgs a) {
         }
         mbar_fence_init();
     }
-    for (int t = threadIdx.x; t < NR * NB * RS; t += BD_PCT) ring[t] = 0.0;
+    // window ring (block b in slot b mod NR): zero, or (spike) unit vectors
+    // in the NSLOT blocks before (FWD) / after (BWD) the chunk
+    for (int t = threadIdx.x; t < NR * NB * RS; t += BD_PCT) {
+        double v = 0.0;
+        if (a.spike) {
+            const int slot = t / (NB * RS), rr = (t / RS) % NB, c = t % RS;
+            const int base = FWD ? s0 - NSLOT : s1;
+            const int wb = ((slot - base) % NR + NR) % NR;
+            v = (wb < NSLOT && c < (BC == 1 ? 1 : ncol) && wb * NB + rr == col0 + c) ? 1.0 : 0.0;
+        }
+        ring[t] = v;
+    }
     __syncthreads();
 
     if (warp == 4) {
         // ---------------- producer ----------------
         if (lane == 0) {
-            const int total = a.nblk * NPB;
+            const int total = nsteps * NPB;
             for (int P = 0; P < total; ++P) {
                 const int buf = P % BD_NBUF, use = P / BD_NBUF;
                 if (use > 0) mbar_wait(&empty[buf], (use - 1) & 1);
@@ -712,7 +728,7 @@ k_band_pipe(BandSolveArgs a) {
 #pragma unroll
         for (int i = 0; i < BPT; ++i) {
             const int cc = bcol + 4 * i;
-            breg[i] = (BC == 1 ? bcol == 0 : cc < ncol)
+            breg[i] = (!a.spike && (BC == 1 ? bcol == 0 : cc < ncol))
                           ? a.Y[(size_t)(col0 + (BC == 1 ? 0 : cc)) * a.ldy + rr] : 0.0;
         }
     };
@@ -723,15 +739,15 @@ k_band_pipe(BandSolveArgs a) {
     };
     load_b(0);
     store_b(0);
-    if (a.nblk > 1) load_b(1);
+    if (nsteps > 1) load_b(1);
     asm volatile("bar.sync 1, 128;" ::: "memory");
 
-    for (int s = 0; s < a.nblk; ++s) {
+    for (int s = 0; s < nsteps; ++s) {
         const int k = blk_of(s);
         const int sbc = s & 1;
-        if (s + 1 < a.nblk) {
+        if (s + 1 < nsteps) {
             store_b(sbc ^ 1);
-            if (s + 2 < a.nblk) load_b(s + 2);
+            if (s + 2 < nsteps) load_b(s + 2);
         }
         // window slot of window block 0 and validity
         const int blk0 = FWD ? (k - NSLOT) : (k + 1);
@@ -777,7 +793,7 @@ k_band_pipe(BandSolveArgs a) {
                     for (int t = 0; t < CW / 4; ++t) {
                         const int jg = jc * CW + 4 * t;     // window row - sub
                         const int wb = jg / NB;
-                        const bool ok = FWD ? (blk0 + wb >= 0) : (blk0 + wb < a.nblk);
+                        const bool ok = FWD ? (blk0 + wb >= lo) : (blk0 + wb < hi);
                         int sl = slot0 + wb; if (sl >= NR) sl -= NR;
                         const double w = ok ? ring[sl * NB + (jg % NB) + sub] : 0.0;
                         f[t % 8] = fma(-Lr[4 * t], w, f[t % 8]);
@@ -788,7 +804,7 @@ k_band_pipe(BandSolveArgs a) {
                     for (int q = 0; q < CW; q += 4) {
                         const int jg = jc * CW + q;     // window row (multiple of 4)
                         const int wb = jg / NB;
-                        const bool ok = FWD ? (blk0 + wb >= 0) : (blk0 + wb < a.nblk);
+                        const bool ok = FWD ? (blk0 + wb >= lo) : (blk0 + wb < hi);
                         int sl = slot0 + wb; if (sl >= NR) sl -= NR;
                         const double av = -Lr[q + q4];
                         const double* rr = ring + ((size_t)sl * NB + (jg % NB) + q4) * RS + g;

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <cublas_v2.h>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -57,7 +58,10 @@ struct Level {
     int4* d_chunks = nullptr;
     int perm_cap = 0;
     // column grouping cache: hash of the inv_dt pattern -> device perm/chunks
-    struct Group { std::vector<double> key; int* perm; int4* chunks; int nch; int BC; };
+    struct Group {
+        std::vector<double> key; int* perm; int4* chunks; int nch; int BC;
+        std::vector<int4> hch;            // host copy of the chunks
+    };
     std::unordered_map<uint64_t, std::vector<Group>> groups;
     Group tmp_group{};
     // SPIKE partition of the chains for latency-bound batches (B <= #SMs)
@@ -95,6 +99,7 @@ struct Level {
 struct pg_ctx {
     int device = 0;
     int n_sm = 148;
+    cublasHandle_t cublas = nullptr;      // SPIKE correction GEMMs (lazy)
     std::vector<Level> levels;
     pg_solver_opts opts{};
     std::string err;
@@ -241,6 +246,7 @@ extern "C" void pg_destroy(pg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     for (auto& L : ctx->levels) free_level(L);
+    if (ctx->cublas) cublasDestroy(ctx->cublas);
     cudaFree(ctx->d_iters);
     cudaFree(ctx->d_ictr);
     for (auto e : ctx->ev) cudaEventDestroy(e);
@@ -307,11 +313,11 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
     L.nblk = (d->n + BD_NB - 1) / BD_NB;
     L.np = L.nblk * BD_NB;
     L.band_ok = L.bwin <= 512;
-    // SPIKE chunks: ~16 chunks of >= max(NSLOT, 8) blocks (windows <= 256)
+    // SPIKE chunks: ~16 chunks of >= max(NSLOT, 8) blocks
     {
         const int nslot = L.bwin / BD_NB;
         L.spk_q = std::max((L.nblk + 15) / 16, std::max(nslot, 8));
-        L.spk_P = L.bwin <= 256 ? L.nblk / L.spk_q : 1;
+        L.spk_P = L.nblk / L.spk_q;
         if (L.spk_P < 2) L.spk_P = 1;
     }
     // rows per tile: 1024 (4 rows per thread); halo from the CSR
@@ -930,9 +936,54 @@ static int ensure_spikes(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
     return band_dir(ctx, L, 8, false, sa, dim3(ng, L.spk_P - 1), sm, st);
 }
 
+// y_p += G_p t_{p-1 / p+1} for every non-first chunk: a plain rank-W GEMM per
+// factor (columns [c0, c1) of the grouped batch), cuBLAS DGEMM (fp64 DMMA)
+static int spike_fix_gemm(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArgs& a,
+                          const std::vector<int4>& hch, cudaStream_t st) {
+    if (!ctx->cublas && cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS)
+        return set_err(ctx, PG_ECUDA, "cublasCreate failed");
+    if (cublasSetStream(ctx->cublas, st) != CUBLAS_STATUS_SUCCESS)
+        return set_err(ctx, PG_ECUDA, "cublasSetStream failed");
+    const double one = 1.0;
+    const int W = a.W, P = a.P, ru = a.q * BD_NB;
+    const int rl = (a.nblk - (P - 1) * a.q) * BD_NB;         // last (longest) chunk
+    const long long sT = (long long)a.ldt * W;
+    const std::vector<double*>& G = fwd ? L.GF : L.GB;
+    for (size_t i = 0; i < hch.size();) {
+        size_t j = i;
+        while (j < hch.size() && hch[j].x == hch[i].x) ++j;
+        const double* Gf = G[hch[i].x];
+        const int c0 = hch[i].y, nc = hch[j - 1].y + hch[j - 1].z - c0;
+        cublasStatus_t cs = CUBLAS_STATUS_SUCCESS;
+        if (fwd) {
+            // chunks 1 .. P-2 (uniform, border of p - 1), then the last
+            if (P > 2)
+                cs = cublasDgemmStridedBatched(
+                    ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ru, nc, W, &one, Gf + ru, a.ldy, ru,
+                    a.T + (size_t)c0 * W, W, sT, &one, a.Y + (size_t)c0 * a.ldy + ru, a.ldy, ru,
+                    P - 2);
+            if (cs == CUBLAS_STATUS_SUCCESS)
+                cs = cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, rl, nc, W, &one,
+                                 Gf + (size_t)(P - 1) * ru, a.ldy,
+                                 a.T + ((size_t)(P - 2) * a.ldt + c0) * W, W, &one,
+                                 a.Y + (size_t)c0 * a.ldy + (size_t)(P - 1) * ru, a.ldy);
+        } else {
+            // chunks 0 .. P-2 (uniform, border of p + 1)
+            cs = cublasDgemmStridedBatched(
+                ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ru, nc, W, &one, Gf, a.ldy, ru,
+                a.T + ((size_t)a.ldt + c0) * W, W, sT, &one, a.Y + (size_t)c0 * a.ldy, a.ldy, ru,
+                P - 1);
+        }
+        if (cs != CUBLAS_STATUS_SUCCESS)
+            return set_err(ctx, PG_ECUDA, "cuBLAS DGEMM failed (status %d)", (int)cs);
+        i = j;                 // (library launches: not counted as ours)
+    }
+    return PG_OK;
+}
+
 template <int BCM>
 static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArgs& a, int nch,
-                           cudaStream_t st) {
+                           const std::vector<int4>& hch, cudaStream_t st) {
     const size_t sm = (size_t)L.bwin * BCM * sizeof(double);
     const size_t smb = sm + (size_t)1024 * BCM * sizeof(double);   // + red[S][BCM][W]
     switch (L.bwin) {
@@ -950,10 +1001,12 @@ static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArg
         PG_BORDER(64)
         PG_BORDER(128)
         PG_BORDER(256)
+        PG_BORDER(512)
 #undef PG_BORDER
         default: return set_err(ctx, PG_EINVAL, "spike window %d not supported", L.bwin);
     }
     LAUNCHED();
+    if (BCM > 1) return spike_fix_gemm(ctx, L, fwd, a, hch, st);
     const int rows = (L.nblk - (L.spk_P - 1) * L.spk_q) * BD_NB;     // longest (last) chunk
     dim3 grid((rows + 255) / 256, L.spk_P - 1, nch);
     if (fwd) k_spike_fix<BCM, true><<<grid, 256, sm, st>>>(a);
@@ -992,7 +1045,8 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         CU(cudaStreamSynchronize(st));
     }
     // latency-bound batches run the SPIKE-partitioned chains
-    const bool spike = L.spk_P > 1 && B <= ctx->n_sm;
+    // (up to ~n_sm/2 column groups of 8: below that the GPU is underfilled)
+    const bool spike = L.spk_P > 1 && B <= 4 * ctx->n_sm;
     const int BC = spike ? (B >= 16 ? 8 : 1) : band_solve_bc(L, B, ctx->n_sm);
     // cached grouping for this exact inv_dt pattern?
     const uint64_t h = hash_doubles(c.data(), B);
@@ -1053,10 +1107,10 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             CU(cudaMemcpyAsync(L.d_chunks, chunks.data(), chunks.size() * sizeof(int4),
                                cudaMemcpyHostToDevice, st));
             CU(cudaStreamSynchronize(st));       // host vectors go out of scope
-            L.tmp_group = Level::Group{c, L.d_perm, L.d_chunks, (int)chunks.size(), BC};
+            L.tmp_group = Level::Group{c, L.d_perm, L.d_chunks, (int)chunks.size(), BC, chunks};
             grp = &L.tmp_group;
         } else {
-            Level::Group gr{c, nullptr, nullptr, (int)chunks.size(), BC};
+            Level::Group gr{c, nullptr, nullptr, (int)chunks.size(), BC, chunks};
             CU(cudaMalloc(&gr.perm, B * sizeof(int)));
             CU(cudaMalloc(&gr.chunks, chunks.size() * sizeof(int4)));
             CU(cudaMemcpy(gr.perm, perm.data(), B * sizeof(int), cudaMemcpyHostToDevice));
@@ -1108,8 +1162,8 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         if ((rc = band_dir(ctx, L, BC, fwd, sa, dim3(nch, P), sm, st))) break;
         if (spike) {
             spa.G = fwd ? L.d_GF : L.d_GB;
-            rc = BC == 1 ? spike_recombine<1>(ctx, L, fwd, spa, nch, st)
-                         : spike_recombine<8>(ctx, L, fwd, spa, nch, st);
+            rc = BC == 1 ? spike_recombine<1>(ctx, L, fwd, spa, nch, grp->hch, st)
+                         : spike_recombine<8>(ctx, L, fwd, spa, nch, grp->hch, st);
         }
     }
     if (rc) return rc;

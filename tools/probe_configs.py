@@ -1,6 +1,6 @@
 """Time-to-solution of BASELINE configs 1-3 at full size on one GPU (dev tool).
 
-usage: python tools/probe_configs.py cfg1|cfg2|cfg2-direct|cfg3 [max_iters]
+usage: python tools/probe_configs.py cfg1|cfg2|cfg2-direct|cfg3|cfg3-window|cfg4[-window][-delayed] [max_iters]
 """
 import json, sys, time
 import numpy as np
@@ -21,9 +21,12 @@ elif name == "cfg3":
     spec = configs.config3(grids=2, strategy="delayed")
 elif name == "cfg3-window":
     spec = configs.config3(n_steps=2 ** 10, grids=2, strategy="delayed")
-elif name in ("cfg4", "cfg4-window"):
-    spec = configs.config4(n_steps=2 ** 12 if name == "cfg4-window" else 2 ** 16)
-    if name == "cfg4-window":
+elif name.startswith("cfg4"):
+    # cfg4, cfg4-window (2^12 steps), cfg4-delayed, cfg4-window-delayed
+    win = "window" in name
+    kw = dict(grids=2, strategy="delayed") if "delayed" in name else {}
+    spec = configs.config4(n_steps=2 ** 12 if win else 2 ** 16, **kw)
+    if win:
         spec["tf"] = spec["tf"] * 2 ** 12 / 2 ** 16
 else:
     raise SystemExit(name)
