@@ -94,6 +94,10 @@ typedef struct pg_solver_opts {
     double  damping;
     int32_t max_halvings;
     double  nu0, k1, k2, k3;    /* nu = nu0 (k1 exp(k2 s^2) + k3) on iron  */
+    double  dt_merge_rtol;      /* banded Cholesky: reuse the factor of an
+                                   existing 1/dt within this relative
+                                   distance (0 = the reference's bitwise
+                                   (level, float(dt)) cache key)           */
 } pg_solver_opts;
 
 /* Per-call statistics (host struct). */

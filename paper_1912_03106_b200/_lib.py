@@ -42,6 +42,7 @@ class SolverOpts(ctypes.Structure):
         ("newton_tol", c_double), ("newton_max_iters", c_int32),
         ("damping", c_double), ("max_halvings", c_int32),
         ("nu0", c_double), ("k1", c_double), ("k2", c_double), ("k3", c_double),
+        ("dt_merge_rtol", c_double),
     ]
 
 

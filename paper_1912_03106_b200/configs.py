@@ -114,6 +114,11 @@ def config3(N=128, n_steps=2 ** 14, levels=3, carrier="triangle", grids=None,
 def config4(N=512, n_steps=2 ** 16, levels=4, carrier="triangle", grids=None,
             strategy="direct"):
     s = config2(N, n_steps, levels, carrier, grids, strategy)
+    # rounding of t_{i+1} - t_i gives ~10 bitwise-distinct dt per level; at
+    # 511^2 every banded factor is 2.4 GB, so factors are shared between 1/dt
+    # values within 1e-12 relative (1e-16-level effect on Phi; the exact
+    # reference cache key is dt_merge_rtol = 0)
+    s["inner"]["dt_merge_rtol"] = 1e-12
     s["name"] = "cfg4"
     return s
 

@@ -48,6 +48,7 @@ struct Level {
     int bw = 0, bwin = 0, LDA = 0, nblk = 0, np = 0;
     bool band_ok = false;
     std::unordered_map<uint64_t, int> fac_index;
+    std::vector<double> fac_c;             // 1/dt of every factor (index = factor id)
     std::vector<double*> FL, FU;
     double** d_FL = nullptr;
     double** d_FU = nullptr;
@@ -266,6 +267,9 @@ extern "C" int pg_set_options(pg_ctx* ctx, const pg_solver_opts* o) {
         return set_err(ctx, PG_EINVAL, "damping must lie in (0, 1], got %g", o->damping);
     if (o->newton_max_iters < 1 || !(o->newton_tol > 0.0))
         return set_err(ctx, PG_EINVAL, "newton max_iters must be >= 1 and tol positive");
+    if (!(o->dt_merge_rtol >= 0.0 && o->dt_merge_rtol < 1e-6))
+        return set_err(ctx, PG_EINVAL, "dt_merge_rtol must lie in [0, 1e-6), got %g",
+                       o->dt_merge_rtol);
     if (o->inner != PG_INNER_PCG && o->inner != PG_INNER_CHOLESKY)
         return set_err(ctx, PG_EINVAL, "inner solver must be PG_INNER_PCG or PG_INNER_CHOLESKY");
     ctx->opts = *o;
@@ -1069,6 +1073,22 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             memcpy(&key, &c[b], 8);
             auto it = L.fac_index.find(key);
             if (it != L.fac_index.end()) { fid[b] = it->second; continue; }
+            if (ctx->opts.dt_merge_rtol > 0.0) {
+                // opt-in: reuse a factor whose 1/dt is within the tolerance
+                // (dt values that differ only by rounding of t_{i+1} - t_i)
+                int hit = -1;
+                for (size_t f = 0; f < L.fac_c.size() && hit < 0; ++f)
+                    if (std::fabs(c[b] - L.fac_c[f]) <= ctx->opts.dt_merge_rtol * std::fabs(L.fac_c[f]))
+                        hit = (int)f;
+                for (size_t f = 0; f < fresh.size() && hit < 0; ++f)
+                    if (std::fabs(c[b] - fresh[f]) <= ctx->opts.dt_merge_rtol * std::fabs(fresh[f]))
+                        hit = (int)(L.FL.size() + f);
+                if (hit >= 0) {
+                    fid[b] = hit;
+                    L.fac_index[key] = hit;
+                    continue;
+                }
+            }
             auto jt = pending.find(key);
             if (jt == pending.end()) {
                 const int id = (int)L.FL.size() + (int)fresh.size();
@@ -1080,6 +1100,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             }
         }
         if ((rc = band_factors(ctx, L, fresh, st))) return rc;
+        L.fac_c.insert(L.fac_c.end(), fresh.begin(), fresh.end());
         for (auto& kv : pending) L.fac_index[kv.first] = kv.second;
         // group columns by factor -> perm, chunks of BC
         std::vector<int> perm(B);

@@ -90,7 +90,8 @@ class GpuFemProblem:
             damping=float(nt.get("damping", 0.5)),
             max_halvings=int(nt.get("max_halvings", 8)),
             nu0=float(spec["nu0"]), k1=float(nl.get("k1", 0.0)),
-            k2=float(nl.get("k2", 0.0)), k3=float(nl.get("k3", 1.0)))
+            k2=float(nl.get("k2", 0.0)), k3=float(nl.get("k3", 1.0)),
+            dt_merge_rtol=float(inner_spec.get("dt_merge_rtol", 0.0)))
         _lib.check(self.ctx, self.lib.pg_set_options(self.ctx, ctypes.byref(self.opts)),
                    "pg_set_options")
         self._weights = [torch.as_tensor(g.weights, device=self.device) for g in self.grids]

@@ -220,3 +220,38 @@ def test_cholesky_wide_band(cuda, N, B):
         exp[idx] = lu.solve(rhs.T).T
     err = np.linalg.norm(got - exp, axis=1) / np.linalg.norm(exp, axis=1)
     assert err.max() < 1e-11, err.max()
+
+
+def test_cholesky_dt_merge_option(cuda):
+    """inner.dt_merge_rtol (opt-in, default 0 = the reference's bitwise
+    float(dt) cache key): 1/dt values one ulp apart share one factor, so the
+    two columns are solved with the same operator; with the option off each
+    keeps its own factor (results differ only at rounding level)."""
+    import copy
+    fx = load_golden("phi_cfg2_n32")
+    spec = copy.deepcopy(fx["spec"])
+    n = (spec["N"] - 1) ** 2
+    rng = np.random.default_rng(11)
+    u = rng.standard_normal(n) * 1e-3
+    U = np.stack([u, u])
+    dt = 0.02 / 2 ** 10
+    inv = np.array([1.0 / dt, np.nextafter(1.0 / dt, 2.0 / dt)])
+    outs = {}
+    for tol in (0.0, 1e-12):
+        spec["inner"]["dt_merge_rtol"] = tol
+        prob = _problem(spec, inner="cholesky")
+        dev = prob.device
+        out = torch.empty(2, n, dtype=torch.float64, device=dev)
+        src = torch.as_tensor(prob.source_values(np.array([0.01, 0.01])), device=dev)
+        prob.phi_batch(0, torch.as_tensor(U, device=dev), torch.as_tensor(inv, device=dev),
+                       src, out)
+        outs[tol] = out.cpu().numpy()
+        prob.close()
+    a, b = outs[0.0], outs[1e-12]
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+    # merged: column 1 used column 0's factor -> differs from column 0 only
+    # through the rhs scaling by its own 1/dt (one ulp)
+    assert np.abs(b[1] - b[0]).max() <= 1e-14 * np.abs(b[0]).max()
+    spec["inner"]["dt_merge_rtol"] = 1e-3
+    with pytest.raises(Exception):
+        _problem(spec, inner="cholesky")

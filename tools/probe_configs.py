@@ -10,7 +10,7 @@ from paper_1912_03106_b200 import (GpuFemProblem, CycleSpec, StoppingCriterion, 
                                    build_uniform_grid, MgritSolver, sequential_solve, configs, build)
 build.build()
 name = sys.argv[1]
-max_iters = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+max_iters = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 50
 if name == "cfg1":
     spec = configs.config1()
 elif name == "cfg2":
@@ -30,6 +30,8 @@ elif name.startswith("cfg4"):
         spec["tf"] = spec["tf"] * 2 ** 12 / 2 ** 16
 else:
     raise SystemExit(name)
+if "merge" in sys.argv[2:]:
+    spec["inner"]["dt_merge_rtol"] = 1e-12
 prob = GpuFemProblem(spec)
 mg = spec["mgrit"]
 grid = build_uniform_grid(0.0, spec["tf"] * spec["n_steps"] / 2 ** 14 if name == "cfg3-window" else spec["tf"], spec["n_steps"])
@@ -49,4 +51,7 @@ print(json.dumps({"config": name, "n": prob.spatial.size(0), "n_steps": spec["n_
                   "history": [run.initial_residual] + run.residual_norms,
                   "phi_columns": run.phi_columns, "inner_iters": st["column_iters"],
                   "newton_iters": st["newton_iters"],
-                  "step_dof_per_s": spec["n_steps"] * prob.spatial.size(0) / t}), flush=True)
+                  "step_dof_per_s": spec["n_steps"] * prob.spatial.size(0) / t,
+                  "dt_merge_rtol": spec["inner"].get("dt_merge_rtol", 0.0),
+                  "gpu_mem_used_gb": (lambda f: (f[1] - f[0]) / 1e9)(torch.cuda.mem_get_info())}),
+      flush=True)
