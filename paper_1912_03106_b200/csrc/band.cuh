@@ -91,6 +91,14 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
     const int stride = a.w + 1;
     const int tid = threadIdx.x;
     auto lb = [&](int i, int j) -> double& { return LB[(size_t)i * stride + (i - j)]; };
+    // unconditional read of band entry (i, j): the address is clamped into the
+    // band so the load never depends on a branch (loads of a row issue together)
+    auto lbv = [&](int i, int j, bool ok) -> double {
+        const int ii = min(i, a.n - 1);
+        const int d = min(max(ii - j, 0), a.w);
+        const double v = LB[(size_t)ii * stride + d];
+        return ok ? v : 0.0;
+    };
 
     for (int k = 0; k < a.nblk; ++k) {
         const int k0 = k * NB;
@@ -98,12 +106,9 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
         // 1. diagonal block (padded with identity beyond n)
         for (int t = tid; t < NB * NB; t += blockDim.x) {
             const int i = t / NB, j = t % NB;
-            double v = 0.0;
-            if (i < kb && j < kb) {
-                if (j <= i && i - j <= a.w) v = lb(k0 + i, k0 + j);
-            } else if (i == j) {
-                v = 1.0;
-            }
+            const bool in = i < kb && j < kb;
+            double v = lbv(k0 + i, k0 + j, in && j <= i && i - j <= a.w);
+            if (!in && i == j) v = 1.0;
             D[i * S + j] = (j <= i) ? v : 0.0;
         }
         __syncthreads();
@@ -142,7 +147,7 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
 #pragma unroll
             for (int j = 0; j < NB; ++j) {
                 const int gc = k0 + j;
-                x[j] = (j < kb && gr - gc <= a.w) ? lb(gr, gc) : 0.0;
+                x[j] = lbv(gr, gc, j < kb && gr - gc <= a.w);
             }
 #pragma unroll
             for (int j = 0; j < NB; ++j) {
@@ -180,7 +185,7 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
                 for (int t = tid; t < NB * CW; t += blockDim.x) {
                     const int i = t / CW, q = c * CW + t % CW;
                     const int gr = k0 + i, gc = k0 - a.W + q;
-                    Lw[t] = (i < kb && gc >= 0 && gr - gc <= a.w) ? lb(gr, gc) : 0.0;
+                    Lw[t] = lbv(gr, max(gc, 0), i < kb && gc >= 0 && gr - gc <= a.w);
                 }
                 __syncthreads();
                 double* flc = fl + NB * BD_PD + (size_t)c * NB * (CW + 4);
