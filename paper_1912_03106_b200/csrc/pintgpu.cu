@@ -101,6 +101,7 @@ struct pg_ctx {
     int device = 0;
     int n_sm = 148;
     cublasHandle_t cublas = nullptr;      // SPIKE correction GEMMs (lazy)
+    int64_t host_iters_last = 0, host_iters_total = 0;   // host-driven (Newton-Krylov) CG iterations
     std::vector<Level> levels;
     pg_solver_opts opts{};
     std::string err;
@@ -1244,6 +1245,7 @@ extern "C" int pg_phi_batch_h(pg_ctx* ctx, int level, int B, const double* u_pre
     cudaStream_t st = (cudaStream_t)stream;
     Level& L = ctx->levels[level];
     ctx->last = pg_phi_stats{};
+    ctx->host_iters_last = 0;
     ctx->last.columns = B;
     ctx->total.columns += B;
     ctx->last_level = level;
@@ -1283,7 +1285,7 @@ extern "C" int pg_last_stats(pg_ctx* ctx, pg_phi_stats* out) {
     int ic[3] = {0, 0, 0};
     CU(cudaMemcpy(it, ctx->d_iters, sizeof it, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(ic, ctx->d_ictr, sizeof ic, cudaMemcpyDeviceToHost));
-    ctx->last.column_iters = (int64_t)it[1];
+    ctx->last.column_iters = (int64_t)it[1] + ctx->host_iters_last;
     ctx->last.batch_iters = ic[0];
     ctx->last.failed = ic[2];
     *out = ctx->last;
@@ -1296,12 +1298,13 @@ extern "C" int pg_total_stats(pg_ctx* ctx, pg_phi_stats* out, int reset) {
     int ic[3] = {0, 0, 0};
     CU(cudaMemcpy(it, ctx->d_iters, sizeof it, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(ic, ctx->d_ictr, sizeof ic, cudaMemcpyDeviceToHost));
-    ctx->total.column_iters = (int64_t)it[0];
+    ctx->total.column_iters = (int64_t)it[0] + ctx->host_iters_total;
     ctx->total.failed = ic[1];
     ctx->total.launches = ctx->launches;
     *out = ctx->total;
     if (reset) {
         ctx->total = pg_phi_stats{};
+        ctx->host_iters_total = 0;
         CU(cudaMemset(ctx->d_iters, 0, 2 * sizeof(unsigned long long)));
         CU(cudaMemset(ctx->d_ictr, 0, 3 * sizeof(int)));
     }
