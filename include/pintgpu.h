@@ -144,6 +144,12 @@ int  pg_phi_batch_h(pg_ctx* ctx, int level, int B,
                     void* stream);
 
 /* Statistics of the most recent pg_phi_batch (synchronises the stream). */
+/* Banded-Cholesky levels: factor every not-yet-cached 1/dt of the list in
+ * one launch (one CTA per factor).  The engine calls it at setup with all
+ * 1/dt of the levels on this grid, so factorisations run in parallel instead
+ * of one launch per first-use.  No-op for Jacobi-PCG. */
+int  pg_prefactor(pg_ctx* ctx, int level, int n, const double* inv_dt_host, void* stream);
+
 int  pg_last_stats(pg_ctx* ctx, pg_phi_stats* out);
 /* Cumulative statistics since the context was created / reset. */
 int  pg_total_stats(pg_ctx* ctx, pg_phi_stats* out, int reset);

@@ -68,6 +68,7 @@ EXPORTS = {
                              c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pg_phi_batch_h": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pg_prefactor": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "pg_last_stats": (c_int, [c_void_p, ctypes.POINTER(PhiStats)]),
     "pg_total_stats": (c_int, [c_void_p, ctypes.POINTER(PhiStats), c_int]),
     "pg_newton_failure": (c_int, [c_void_p, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),

@@ -1031,6 +1031,51 @@ static uint64_t hash_doubles(const double* v, int n) {
     return h;
 }
 
+// Factor index of every 1/dt in c[0..n) (cached per bitwise value of 1/dt,
+// like the reference's (grid, float(dt)) cache; opt-in tolerance sharing),
+// all new factors in one launch.
+static int factor_ids(pg_ctx* ctx, Level& L, const double* c, int n, int* fid,
+                      cudaStream_t st) {
+    std::vector<double> fresh;
+    std::unordered_map<uint64_t, int> pending;
+    for (int b = 0; b < n; ++b) {
+        uint64_t key;
+        memcpy(&key, &c[b], 8);
+        auto it = L.fac_index.find(key);
+        if (it != L.fac_index.end()) { fid[b] = it->second; continue; }
+        if (ctx->opts.dt_merge_rtol > 0.0) {
+            // reuse a factor whose 1/dt is within the tolerance (dt values
+            // that differ only by rounding of t_{i+1} - t_i)
+            int hit = -1;
+            for (size_t f = 0; f < L.fac_c.size() && hit < 0; ++f)
+                if (std::fabs(c[b] - L.fac_c[f]) <= ctx->opts.dt_merge_rtol * std::fabs(L.fac_c[f]))
+                    hit = (int)f;
+            for (size_t f = 0; f < fresh.size() && hit < 0; ++f)
+                if (std::fabs(c[b] - fresh[f]) <= ctx->opts.dt_merge_rtol * std::fabs(fresh[f]))
+                    hit = (int)(L.FL.size() + f);
+            if (hit >= 0) {
+                fid[b] = hit;
+                L.fac_index[key] = hit;
+                continue;
+            }
+        }
+        auto jt = pending.find(key);
+        if (jt == pending.end()) {
+            const int id = (int)L.FL.size() + (int)fresh.size();
+            pending[key] = id;
+            fresh.push_back(c[b]);
+            fid[b] = id;
+        } else {
+            fid[b] = jt->second;
+        }
+    }
+    int rc = band_factors(ctx, L, fresh, st);
+    if (rc) return rc;
+    L.fac_c.insert(L.fac_c.end(), fresh.begin(), fresh.end());
+    for (auto& kv : pending) L.fac_index[kv.first] = kv.second;
+    return PG_OK;
+}
+
 // Banded-Cholesky solve of B columns.  Default: Phi (rhs = c M u_prev + f,
 // columns 0..B-1).  Preconditioner mode (copy_src != NULL): the rhs of
 // column j is copy_src[sub[j]], the result goes to u_out[sub[j]] (sub: host
@@ -1064,45 +1109,8 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     int rc;
     std::vector<int> fid;
     if (!grp) {
-        // factor index per column (cached per bitwise value of 1/dt, like the
-        // reference's (grid, float(dt)) cache), new factors in one launch
         fid.resize(B);
-        std::vector<double> fresh;
-        std::unordered_map<uint64_t, int> pending;
-        for (int b = 0; b < B; ++b) {
-            uint64_t key;
-            memcpy(&key, &c[b], 8);
-            auto it = L.fac_index.find(key);
-            if (it != L.fac_index.end()) { fid[b] = it->second; continue; }
-            if (ctx->opts.dt_merge_rtol > 0.0) {
-                // opt-in: reuse a factor whose 1/dt is within the tolerance
-                // (dt values that differ only by rounding of t_{i+1} - t_i)
-                int hit = -1;
-                for (size_t f = 0; f < L.fac_c.size() && hit < 0; ++f)
-                    if (std::fabs(c[b] - L.fac_c[f]) <= ctx->opts.dt_merge_rtol * std::fabs(L.fac_c[f]))
-                        hit = (int)f;
-                for (size_t f = 0; f < fresh.size() && hit < 0; ++f)
-                    if (std::fabs(c[b] - fresh[f]) <= ctx->opts.dt_merge_rtol * std::fabs(fresh[f]))
-                        hit = (int)(L.FL.size() + f);
-                if (hit >= 0) {
-                    fid[b] = hit;
-                    L.fac_index[key] = hit;
-                    continue;
-                }
-            }
-            auto jt = pending.find(key);
-            if (jt == pending.end()) {
-                const int id = (int)L.FL.size() + (int)fresh.size();
-                pending[key] = id;
-                fresh.push_back(c[b]);
-                fid[b] = id;
-            } else {
-                fid[b] = jt->second;
-            }
-        }
-        if ((rc = band_factors(ctx, L, fresh, st))) return rc;
-        L.fac_c.insert(L.fac_c.end(), fresh.begin(), fresh.end());
-        for (auto& kv : pending) L.fac_index[kv.first] = kv.second;
+        if ((rc = factor_ids(ctx, L, c.data(), B, fid.data(), st))) return rc;
         // group columns by factor -> perm, chunks of BC
         std::vector<int> perm(B);
         for (int b = 0; b < B; ++b) perm[b] = b;
@@ -1216,6 +1224,20 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     k_band_scatter<<<gs, 256, 0, st>>>(L.n, L.np, L.Y, d_perm, u_out, g, g_idx);
     LAUNCHED();
     return PG_OK;
+}
+
+extern "C" int pg_prefactor(pg_ctx* ctx, int level, int n, const double* inv_dt_host,
+                            void* stream) {
+    if (!ctx) return PG_EINVAL;
+    if (level < 0 || level >= (int)ctx->levels.size())
+        return set_err(ctx, PG_EINVAL, "no spatial level %d", level);
+    if (n < 0 || (n > 0 && !inv_dt_host)) return set_err(ctx, PG_EINVAL, "bad 1/dt list");
+    Level& L = ctx->levels[level];
+    if (ctx->opts.inner != PG_INNER_CHOLESKY || !L.band_ok || n == 0) return PG_OK;
+    if (L.n_elem > 0 && !L.k_pre) return PG_OK;
+    CU(cudaSetDevice(ctx->device));
+    std::vector<int> fid(n);
+    return factor_ids(ctx, L, inv_dt_host, n, fid.data(), (cudaStream_t)stream);
 }
 
 extern "C" int pg_phi_batch(pg_ctx* ctx, int level, int B, const double* u_prev,

@@ -225,6 +225,13 @@ class MgritSolver:
             lvl.lkept = torch.zeros(lvl.K, nxt.n, **f64)
             lvl.cprop = torch.zeros(lvl.K, nxt.n, **f64)
             lvl.crhs = torch.zeros(lvl.K, nxt.n, **f64)
+        # every distinct 1/dt of the levels on a grid, factored in one launch
+        # per grid at setup (banded Cholesky) instead of at first use
+        if hasattr(problem, "prefactor"):
+            for s_lvl in sorted(set(self.assignment[:n_levels])):
+                vals = [lv.inv_dt_all_h[1:] for lv in self.levels if lv.s == s_lvl]
+                if vals:
+                    problem.prefactor(s_lvl, np.unique(np.concatenate(vals)))
         self._plans = {}
         self._smooth = False
         import inspect

@@ -212,6 +212,14 @@ class GpuFemProblem:
             raise NewtonConvergenceError(msg, time=None, iterations=its.value)
         _lib.check(self.ctx, rc, "pg_phi_batch")
 
+    def prefactor(self, level, inv_dt_host):
+        """Factor every distinct 1/dt of the list up front (banded Cholesky;
+        one launch, one CTA per factor)."""
+        arr = np.ascontiguousarray(np.asarray(inv_dt_host, dtype=np.float64))
+        _lib.check(self.ctx, self.lib.pg_prefactor(
+            self.ctx, int(level), int(arr.size), arr.ctypes.data_as(ctypes.c_void_p),
+            self._stream()), "pg_prefactor")
+
     def last_stats(self):
         s = _lib.PhiStats()
         _lib.check(self.ctx, self.lib.pg_last_stats(self.ctx, ctypes.byref(s)), "pg_last_stats")
