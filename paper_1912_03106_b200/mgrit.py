@@ -234,6 +234,7 @@ class MgritSolver:
                     problem.prefactor(s_lvl, np.unique(np.concatenate(vals)))
         self._plans = {}
         self._smooth = False
+        self._probe_prop = None      # probe result reusable by the next level-0 FC sweep
         import inspect
         self._takes_host_dt = "inv_dt_host" in inspect.signature(problem.phi_batch).parameters
         self.phi_columns = 0
@@ -314,6 +315,16 @@ class MgritSolver:
     # --- sweeps ---
     def _fc_sweep(self, lvl):
         """mgrit.py:378-393"""
+        if lvl.index == 0 and self._probe_prop is not None:
+            # The residual probe that precedes every cycle ran exactly this
+            # F-walk and C-step from the same pre-sweep C-values (and sent the
+            # same boundary): its propagated C-values are this sweep's result,
+            # bit for bit, so the sweep is not recomputed.
+            prop, self._probe_prop = self._probe_prop, None
+            if prop is not False:
+                lvl.c_store.copy_(prop)
+            return
+        self._probe_prop = None
         boundary = self._exchange_left(lvl)
         if lvl.empty or not lvl.K:
             return
@@ -334,6 +345,7 @@ class MgritSolver:
 
     def _restrict_sweep(self, lvl, nxt):
         """mgrit.py:395-450"""
+        self._probe_prop = None
         prob = self.problem
         coarsen = nxt.s != lvl.s
         boundary = self._exchange_left(lvl)
@@ -445,6 +457,7 @@ class MgritSolver:
     def _ascend(self, coarse, fine, inject=False, solved=False):
         """mgrit.py:497-571: coarse walk (unless solved) turning u_keep into
         the payload v - kept (or v), then delivery to the fine C-store."""
+        self._probe_prop = None
         prob = self.problem
         if not coarse.empty and not solved:
             boundary = self._exchange_left(coarse)
@@ -521,11 +534,16 @@ class MgritSolver:
         """mgrit.py:573-598: residual and per-C losses, state untouched."""
         prob = self.problem
         boundary = self._exchange_left(lvl)
+        # idle ranks mark the reuse too, so every rank skips the same exchange
+        self._probe_prop = (False if (lvl.index == 0 and not self._smooth and not lvl.use_rhs)
+                            else None)
         if lvl.empty or not lvl.K:
             return 0.0, np.zeros(0)
         last_f = self._walk(lvl, self._starts(lvl, boundary))
         prop = self._other(lvl, last_f)
         self._phi_off(lvl, last_f, lvl.m, prop, add_rhs=False)
+        if lvl.index == 0 and not lvl.use_rhs and not self._smooth:
+            self._probe_prop = prop          # = the next cycle's first C-relaxation
         use_g = lvl.use_rhs
         prob.c_residual(lvl.s, prop, lvl.c_store, lvl.sumsq,
                         g=lvl.rhs if use_g else None,
@@ -571,6 +589,7 @@ class MgritSolver:
 
     def _coarsest_solve_single(self):
         """mgrit.py:637-655: sequential walk depositing C-values."""
+        self._probe_prop = None
         lvl = self.levels[0]
         if lvl.empty:
             return
