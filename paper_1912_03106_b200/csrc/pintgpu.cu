@@ -102,6 +102,7 @@ struct pg_ctx {
     int n_sm = 148;
     cublasHandle_t cublas = nullptr;      // SPIKE correction GEMMs (lazy)
     int64_t host_iters_last = 0, host_iters_total = 0;   // host-driven (Newton-Krylov) CG iterations
+    bool dev_stats_last = false;          // last call used the device counters
     std::vector<Level> levels;
     pg_solver_opts opts{};
     std::string err;
@@ -1164,16 +1165,9 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     LAUNCHED();
     const int P = spike ? L.spk_P : 1;
     if (spike) {
-        std::vector<char> need(L.FL.size(), 0);
-        for (int b = 0; b < B; ++b) need[fid.empty() ? 0 : fid[b]] = 1;
-        if (fid.empty()) {                 // cached grouping: factors from the chunks
-            std::vector<int4> hch(nch);
-            CU(cudaMemcpy(hch.data(), d_chunks, nch * sizeof(int4), cudaMemcpyDeviceToHost));
-            std::fill(need.begin(), need.end(), 0);
-            for (const int4& q : hch) need[q.x] = 1;
-        }
-        for (size_t f = 0; f < need.size(); ++f)
-            if (need[f] && (rc = ensure_spikes(ctx, L, (int)f, st))) return rc;
+        // factors of this call (host copy of the chunks: no device round trip)
+        for (const int4& q : grp->hch)
+            if (!L.GF[q.x] && (rc = ensure_spikes(ctx, L, q.x, st))) return rc;
         const size_t tneed = (size_t)P * L.bwin * B;
         if (tneed > L.spk_T_cap) {
             if (L.spk_T) cudaFree(L.spk_T);
@@ -1203,9 +1197,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         // 2 * 2 * np * (W + nb) flops; HBM bytes = Y in/out twice + each
         // distinct factor pair read once
         std::vector<char> used(L.FL.size(), 0);
-        std::vector<int4> hch(nch);
-        CU(cudaMemcpy(hch.data(), d_chunks, nch * sizeof(int4), cudaMemcpyDeviceToHost));
-        for (const int4& q : hch) used[q.x] = 1;
+        for (const int4& q : grp->hch) used[q.x] = 1;
         double fb = 0.0;
         for (char u : used) fb += u ? 2.0 * bd_block_doubles(L.bwin) * L.nblk * 8.0 : 0.0;
         ctx->prof_flops[2] += 4.0 * L.np * (double)(L.bwin + BD_NB) * B;
@@ -1273,7 +1265,12 @@ extern "C" int pg_phi_batch_h(pg_ctx* ctx, int level, int B, const double* u_pre
     ctx->last_level = level;
     int rc = ensure_ws(ctx, L, B);
     if (rc) return rc;
-    if ((rc = begin_stats(ctx, L, st))) return rc;
+    // device iteration counters: only the PCG / in-kernel Newton paths use
+    // them (the banded and Newton-Krylov paths skip the per-call resets)
+    const bool dev_stats = !(ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok &&
+                             (L.n_elem == 0 || L.k_pre));
+    ctx->dev_stats_last = dev_stats;
+    if (dev_stats && (rc = begin_stats(ctx, L, st))) return rc;
     if (L.n_elem > 0 && ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok && L.k_pre) {
         return newton_nk(ctx, L, B, u_prev, guess, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
     }
@@ -1307,6 +1304,7 @@ extern "C" int pg_last_stats(pg_ctx* ctx, pg_phi_stats* out) {
     int ic[3] = {0, 0, 0};
     CU(cudaMemcpy(it, ctx->d_iters, sizeof it, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(ic, ctx->d_ictr, sizeof ic, cudaMemcpyDeviceToHost));
+    if (!ctx->dev_stats_last) it[1] = 0, ic[0] = 1, ic[2] = 0;   // direct solve: 1 (problems.py:146)
     ctx->last.column_iters = (int64_t)it[1] + ctx->host_iters_last;
     ctx->last.batch_iters = ic[0];
     ctx->last.failed = ic[2];

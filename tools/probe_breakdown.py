@@ -9,6 +9,8 @@ build.build()
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 spec = (configs.config2(grids=2, strategy="delayed") if name == "cfg2"
         else configs.config3(grids=2, strategy="delayed"))
+if "merge" in sys.argv[2:]:
+    spec["inner"]["dt_merge_rtol"] = 1e-12
 prob = GpuFemProblem(spec)
 mg = spec["mgrit"]
 grid = build_uniform_grid(0.0, spec["tf"], spec["n_steps"])
@@ -47,7 +49,8 @@ for lv, B, e0, e1 in rec:
     a[0] += 1
     a[1] += e0.elapsed_time(e1)
 tot = sum(v[1] for v in agg.values())
-print(json.dumps({"wall_s": wall, "iterations": run.iterations, "phi_ms": tot}))
+print(json.dumps({"wall_s": wall, "iterations": run.iterations, "phi_ms": tot,
+                  "history": [run.initial_residual] + run.residual_norms}))
 for k in sorted(agg, key=lambda k: -agg[k][1]):
     n, ms = agg[k]
     print(f"grid {k[0]} B={k[1]:5d}: {n:5d} calls, {ms:8.1f} ms, {ms / n * 1e3:7.0f} us/call")
