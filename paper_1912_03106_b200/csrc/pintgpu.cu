@@ -1012,7 +1012,11 @@ static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArg
         default: return set_err(ctx, PG_EINVAL, "spike window %d not supported", L.bwin);
     }
     LAUNCHED();
-    if (BCM > 1) return spike_fix_gemm(ctx, L, fwd, a, hch, st);
+    // one GEMM per factor pays off for few, wide factor groups; many narrow
+    // groups (bitwise-distinct dt of one level) go through one fused launch
+    int groups = 0;
+    for (size_t i = 0; i < hch.size(); ++i) groups += (i == 0 || hch[i].x != hch[i - 1].x);
+    if (BCM > 1 && groups <= 2) return spike_fix_gemm(ctx, L, fwd, a, hch, st);
     const int rows = (L.nblk - (L.spk_P - 1) * L.spk_q) * BD_NB;     // longest (last) chunk
     dim3 grid((rows + 255) / 256, L.spk_P - 1, nch);
     if (fwd) k_spike_fix<BCM, true><<<grid, 256, sm, st>>>(a);
