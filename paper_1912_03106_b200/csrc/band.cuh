@@ -26,6 +26,7 @@
 #include "tma.cuh"
 
 #define BD_NB 32
+#define BD_RHS_SRC 8          // source shapes held in registers by the rhs kernels
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
     asm volatile(
@@ -236,6 +237,19 @@ struct BandSolveArgs {
     // the window before (FWD) / after (BWD) the chunk starts as unit vectors
     // (column c of the chunk group = window index col0 + c).
     int q, P, p0, spike;
+    // k_band_chain_ks only: the scatter fused into the backward chain (x
+    // written straight to u_out (+ g), skipping a [B][n] pass over HBM).
+    // Zero-initialised = off.  (Forming b = c M u + f inside the forward
+    // chain was measured 1.9x slower: the stencil loads compete with the
+    // chain's shared-memory operand stream for the LSU pipe.)
+    struct Fuse {
+        int scatter;
+        int n;
+        const int* perm;                 // grouped column -> batch column
+        double* u_out;                   // [B][n]
+        const double* g;                 // optional [*][n], row g_idx[b]
+        const int* g_idx;
+    } fz;
 };
 
 // The sequential chain:  y_k = D_k^-1 b_k - (D_k^-1 L_win) y_window
@@ -388,6 +402,221 @@ k_band_chain(BandSolveArgs a) {
                 if (cc < ncol) a.Y[(size_t)(col0 + cc) * a.ldy + row] = v;
             }
         __syncthreads();            // block k visible in the ring; stage / sb buffers free
+    }
+}
+
+// k-split chain: the same block step as k_band_chain with the 40 (W = 128)
+// k-steps of every 8-row tile split between KS warps, so each SM
+// sub-partition runs KS warps: while one waits for its DMMA issue slot the
+// others issue their shared-memory loads (a single warp per sub-partition
+// serialises DMMA issue, LDS latency and index math -- measured 1,665 cycles
+// per step against 720 of DMMA issue).  128 KS threads: warp w owns rows
+// 8 (w & 3) .. + 7 and k-slice w >> 2 of the block's k-steps (k-step t < 8:
+// D^-1 b_k, t >= 8: window columns 4 (t - 8) ..).  Slices 1.. hand their
+// partial tiles to slice 0 through shared memory under a named barrier per
+// row tile; slice 0 finishes the block.
+#include <type_traits>
+#ifndef BD_KS_NCH
+#define BD_KS_NCH 2
+#endif
+template <int BC, int CW, int NCHK, bool FWD, int KS>
+__global__ void __launch_bounds__(128 * KS)
+k_band_chain_ks(BandSolveArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t bar[BD_NST];
+    constexpr int NT = 128 * KS;
+    constexpr int NST = BD_NST;
+    constexpr int NSLOT = CW * NCHK / BD_NB;
+    constexpr int BLK = BD_NB * (BD_PD + NCHK * (CW + 4));
+    constexpr int NB = BD_NB, RS = BC + 4, NT8 = BC / 8;
+    constexpr int W = NSLOT * NB;
+    constexpr int RMASK = 2 * NSLOT - 1;
+    constexpr int KT = NB / 4 + W / 4;                  // k-steps per block step
+    static_assert(KT % KS == 0, "k-steps must split evenly");
+    constexpr int KPS = KT / KS;                        // k-steps per slice
+    // DMMA latency ~27 cycles vs ~16 per issue: two chains keep the pipe busy
+    constexpr int NCH = KPS >= 4 ? BD_KS_NCH : 1;
+    __shared__ __align__(16) double part[KS > 1 ? KS - 1 : 1][4][32][2 * NT8];
+    const int4 ch = a.chunks[blockIdx.x];
+    const double* F = a.F[ch.x];
+    const int col0 = ch.y, ncol = ch.z;
+    double* stage = sm;
+    double* ring = stage + (size_t)NST * BLK;
+    double* sb = ring + (size_t)2 * NSLOT * NB * RS;   // [2][NB][RS]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mt = warp & 3, kh = warp >> 2;
+    const int g = lane >> 2, q4 = lane & 3;
+    const int lrow = 8 * mt + g;
+    const uint32_t blk_bytes = (uint32_t)(BLK * 8);
+    // b staging: thread t moves (row t & 31, columns (t >> 5) + (NT / 32) j)
+    constexpr int CST = NT / 32;
+    constexpr int BPT = (BC + CST - 1) / CST;
+    const int brow = threadIdx.x & 31, bcol = threadIdx.x >> 5;
+
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < NST; ++q) mbar_init(&bar[q], 1);
+        mbar_fence_init();
+    }
+    const int pch = a.p0 + blockIdx.y;
+    const int s0 = pch * a.q;
+    const int s1 = pch + 1 == a.P ? a.nblk : s0 + a.q;
+    const int nsteps = s1 - s0;
+    const int lo = s0 - (a.spike ? NSLOT : 0), hi = s1 + (a.spike ? NSLOT : 0);
+    auto blk_of = [&](int s) { return FWD ? s0 + s : s1 - 1 - s; };
+    for (int t = threadIdx.x; t < 2 * NSLOT * NB * RS; t += NT) {
+        double v = 0.0;
+        if (a.spike) {
+            const int slot = t / (NB * RS), rr = (t / RS) % NB, c = t % RS;
+            const int wb = (slot - (FWD ? s0 - NSLOT : s1)) & RMASK;
+            v = (wb < NSLOT && c < ncol && wb * NB + rr == col0 + c) ? 1.0 : 0.0;
+        }
+        ring[t] = v;
+    }
+    double breg[BPT];
+    auto load_b = [&](int s) {
+        const int rr = NB * blk_of(s) + brow;
+#pragma unroll
+        for (int j = 0; j < BPT; ++j) {
+            const int cc = bcol + CST * j;
+            breg[j] = (!a.spike && cc < ncol) ? a.Y[(size_t)(col0 + cc) * a.ldy + rr] : 0.0;
+        }
+    };
+    auto store_b = [&](int buf) {
+#pragma unroll
+        for (int j = 0; j < BPT; ++j)
+            if (bcol + CST * j < BC) sb[((size_t)buf * NB + brow) * RS + bcol + CST * j] = breg[j];
+    };
+    // fused scatter (BWD, unpartitioned chain): output pointers of this
+    // thread's (row, column) entries, resolved once
+    const bool fsc = !FWD && a.fz.scatter && a.P == 1 && !a.spike;
+    double* fo[NT8][2];
+    const double* fg[NT8][2];
+    if (fsc && kh == 0) {
+#pragma unroll
+        for (int nt = 0; nt < NT8; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cc = 8 * nt + 2 * q4 + h;
+                const int b = cc < ncol ? a.fz.perm[col0 + cc] : -1;
+                fo[nt][h] = b >= 0 ? a.fz.u_out + (size_t)b * a.fz.n : nullptr;
+                const int gi = (b >= 0 && a.fz.g) ? a.fz.g_idx[b] : -1;
+                fg[nt][h] = gi >= 0 ? a.fz.g + (size_t)gi * a.fz.n : nullptr;
+            }
+    }
+    load_b(0);
+    store_b(0);
+    if (nsteps > 1) load_b(1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 0; q + 1 < NST && q < nsteps; ++q) {
+            mbar_arrive_expect_tx(&bar[q], blk_bytes);
+            tma_load_1d(stage + (size_t)q * BLK, F + (size_t)blk_of(q) * BLK, blk_bytes, &bar[q]);
+        }
+    }
+    for (int s = 0; s < nsteps; ++s) {
+        const int k = blk_of(s);
+        const int st = s & 1;
+        const int sb_cur = s & 1;
+        if (threadIdx.x == 0 && s + NST - 1 < nsteps) {
+            const int sn = (s + 1) & 1;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bar[sn], blk_bytes);
+            tma_load_1d(stage + (size_t)sn * BLK, F + (size_t)blk_of(s + NST - 1) * BLK,
+                        blk_bytes, &bar[sn]);
+        }
+        if (s + 1 < nsteps) {
+            store_b(sb_cur ^ 1);
+            if (s + 2 < nsteps) load_b(s + 2);
+        }
+        double acc[NCH][NT8][2];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
+        mbar_wait(&bar[st], (s >> 1) & 1);
+        const double* Lst = stage + (size_t)st * BLK;
+        const double* bb = sb + (size_t)sb_cur * NB * RS;
+        // this warp's k-slice; the slice index is made a compile-time constant
+        // so every operand address below folds to base + immediate
+        auto slice = [&](auto KHC) {
+            constexpr int KH = decltype(KHC)::value;
+#pragma unroll
+            for (int u = 0; u < KPS; ++u) {
+                const int t = KH * KPS + u;
+                double av;
+                const double* rr;
+                bool ok = true;
+                if (t < NB / 4) {                       // D_k^-1 b_k
+                    av = Lst[lrow * BD_PD + 4 * t + q4];
+                    rr = bb + (4 * t + q4) * RS + g;
+                } else {                                // - (D_k^-1 L_win) y_window
+                    const int j = 4 * (t - NB / 4);
+                    const int wbi = j / NB;
+                    const int blk = FWD ? (k - NSLOT + wbi) : (k + 1 + wbi);
+                    ok = FWD ? (blk >= lo) : (blk < hi);
+                    av = -Lst[NB * BD_PD + (j / CW) * NB * (CW + 4) + lrow * (CW + 4) +
+                              (j % CW) + q4];
+                    rr = ring + ((size_t)(blk & RMASK) * NB + (j % NB) + q4) * RS + g;
+                }
+#pragma unroll
+                for (int nt = 0; nt < NT8; ++nt) {
+                    const double bv = ok ? rr[8 * nt] : 0.0;
+                    dmma_8x8x4(acc[u % NCH][nt][0], acc[u % NCH][nt][1], av, bv);
+                }
+            }
+        };
+        if constexpr (KS == 1) {
+            slice(std::integral_constant<int, 0>{});
+        } else {
+            switch (kh) {
+                case 0: slice(std::integral_constant<int, 0>{}); break;
+                case 1: slice(std::integral_constant<int, 1>{}); break;
+                case 2: if constexpr (KS > 2) slice(std::integral_constant<int, (KS > 2 ? 2 : 0)>{}); break;
+                default: if constexpr (KS > 3) slice(std::integral_constant<int, (KS > 3 ? 3 : 0)>{}); break;
+            }
+        }
+        double v[NT8][2];
+#pragma unroll
+        for (int nt = 0; nt < NT8; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double x = acc[0][nt][h];
+#pragma unroll
+                for (int c = 1; c < NCH; ++c) x += acc[c][nt][h];
+                v[nt][h] = x;
+            }
+        if constexpr (KS > 1) {
+            if (kh > 0) {
+#pragma unroll
+                for (int nt = 0; nt < NT8; ++nt) {
+                    part[kh - 1][mt][lane][2 * nt] = v[nt][0];
+                    part[kh - 1][mt][lane][2 * nt + 1] = v[nt][1];
+                }
+            }
+            // the KS warps of row tile mt: named barrier 1 + mt
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + mt), "r"(32 * KS) : "memory");
+        }
+        if (kh == 0) {
+            double* slotp = ring + (size_t)(k & RMASK) * NB * RS;
+            const int row = NB * k + lrow;
+#pragma unroll
+            for (int nt = 0; nt < NT8; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cc = 8 * nt + 2 * q4 + h;
+                    double y = v[nt][h];
+#pragma unroll
+                    for (int q = 0; q < KS - 1; ++q) y += part[q][mt][lane][2 * nt + h];
+                    slotp[lrow * RS + cc] = y;
+                    if (fsc) {
+                        if (fo[nt][h] && row < a.fz.n)
+                            fo[nt][h][row] = fg[nt][h] ? y + fg[nt][h][row] : y;
+                    } else if (cc < ncol) {
+                        a.Y[(size_t)(col0 + cc) * a.ldy + row] = y;
+                    }
+                }
+        }
+        __syncthreads();            // block k visible in the ring; stage / sb / part free
     }
 }
 
@@ -917,6 +1146,79 @@ k_band_rhs(int n, int ldy, int B, const int* __restrict__ row_ptr,
 #pragma unroll
         for (int j = 0; j < BD_RHS_CB; ++j)
             if (j < ncol) yb[j][i] = acc[j];
+    }
+}
+
+// b = c M u + f on the symmetric DIA copy of M (structured stencils).  One
+// thread per row; the row's M diagonals and source shapes stay in registers
+// while the thread walks BD_RHS_CC columns, whose perm / 1/dt / source values
+// sit in shared memory (broadcast reads).  Per output: 7 coalesced u loads
+// (neighbours hit L1/L2), one store -- 16 n bytes of HBM per column.
+#define BD_RHS_CC 32
+struct RhsDia {
+    int n, ldy, B, U, n_src;
+    int off[5];
+    const double2* __restrict__ mk;      // [(U+1)][n] (m, k); lower = mirrored upper
+    const double* __restrict__ shapes;   // [n_src][n]
+};
+__global__ void __launch_bounds__(256)
+k_band_rhs_dia(RhsDia a, const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
+               const double* __restrict__ src, const int* __restrict__ perm,
+               double* __restrict__ Y) {
+    __shared__ int sp[BD_RHS_CC];
+    __shared__ double sc[BD_RHS_CC], ss[BD_RHS_CC][BD_RHS_SRC];
+    const int gc0 = blockIdx.y * BD_RHS_CC;
+    const int ncol = min(BD_RHS_CC, a.B - gc0);
+    for (int t = threadIdx.x; t < BD_RHS_CC * BD_RHS_SRC; t += blockDim.x) {
+        const int j = t / BD_RHS_SRC, q = t % BD_RHS_SRC;
+        const int b = j < ncol ? perm[gc0 + j] : 0;
+        if (q == 0) {
+            sp[j] = b;
+            sc[j] = j < ncol ? inv_dt[b] : 0.0;
+        }
+        ss[j][q] = (j < ncol && q < a.n_src) ? src[(size_t)b * a.n_src + q] : 0.0;
+    }
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.ldy) return;
+    if (i >= a.n) {
+        for (int j = 0; j < ncol; ++j) Y[(size_t)(gc0 + j) * a.ldy + i] = 0.0;
+        return;
+    }
+    double mup[4], mlo[4];
+    int oup[4], olo[4];
+    const double m0 = a.mk[i].x;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int o = a.off[u + 1];
+        const bool on = u < a.U;
+        const bool hu = on && i + o < a.n, hl = on && i - o >= 0;
+        mup[u] = hu ? a.mk[(size_t)(u + 1) * a.n + i].x : 0.0;
+        mlo[u] = hl ? a.mk[(size_t)(u + 1) * a.n + i - o].x : 0.0;
+        oup[u] = hu ? o : 0;               // in-range dummy offset when absent
+        olo[u] = hl ? -o : 0;
+    }
+    double sh[BD_RHS_SRC];
+#pragma unroll
+    for (int q = 0; q < BD_RHS_SRC; ++q) sh[q] = q < a.n_src ? a.shapes[(size_t)q * a.n + i] : 0.0;
+    // the slot boxes cover a few % of the rows: rows outside every shape skip
+    // the source term (warp-uniform away from the box edges)
+    bool has_src = false;
+#pragma unroll
+    for (int q = 0; q < BD_RHS_SRC; ++q) has_src |= sh[q] != 0.0;
+    double* yo = Y + (size_t)gc0 * a.ldy + i;
+#pragma unroll 4
+    for (int j = 0; j < ncol; ++j) {
+        const double* ub = u_prev + (size_t)sp[j] * a.n + i;
+        double v = m0 * ub[0];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v = fma(mup[u], ub[oup[u]], fma(mlo[u], ub[olo[u]], v));
+        double f = 0.0;
+        if (has_src) {
+#pragma unroll
+            for (int q = 0; q < BD_RHS_SRC; ++q) f = fma(ss[j][q], sh[q], f);
+        }
+        yo[(size_t)j * a.ldy] = fma(sc[j], v, f);
     }
 }
 

@@ -319,11 +319,16 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
     L.nblk = (d->n + BD_NB - 1) / BD_NB;
     L.np = L.nblk * BD_NB;
     L.band_ok = L.bwin <= 512;
-    // SPIKE chunks: ~16 chunks of >= max(NSLOT, 8) blocks
+    // SPIKE chunks: ~8 chunks of >= max(NSLOT, 8) blocks
     {
         const int nslot = L.bwin / BD_NB;
-        L.spk_q = std::max((L.nblk + 15) / 16, std::max(nslot, 8));
-        L.spk_P = L.nblk / L.spk_q;
+        int target = 8;          // measured on config 2: 8 chunks beat 4, 6, 12, 16, 24, 32
+        if (const char* e = getenv("PG_SPIKE_CHUNKS")) target = std::max(2, atoi(e));  // dev A/B
+        L.spk_q = std::max((L.nblk + target - 1) / target, std::max(nslot, 8));
+        // balanced: ceil, with the remainder as a shorter last chunk (it still
+        // holds >= NSLOT blocks: its head is the border of the chunk before)
+        L.spk_P = (L.nblk + L.spk_q - 1) / L.spk_q;
+        if (L.nblk - (L.spk_P - 1) * L.spk_q < nslot) --L.spk_P;
         if (L.spk_P < 2) L.spk_P = 1;
     }
     // rows per tile: 1024 (4 rows per thread); halo from the CSR
@@ -785,12 +790,29 @@ static int newton_nk(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
 // over ~B/8 SMs; 16 when the batch is large enough to fill the GPU anyway.
 static int band_solve_bc(const Level& L, int B, int n_sm) {
     if (B <= n_sm) return 1;          // one column per CTA: FMA chain
+    if (const char* e = getenv("PG_BAND_BC")) {          // dev override (A/B measurements)
+        const int v = atoi(e);
+        if (v == 8 || (v == 16 && L.bwin <= 256)) return v;
+    }
     if (L.bwin >= 512) return 8;      // 17-slot window ring leaves room for 8
     return B >= 16 * n_sm ? 16 : 8;
 }
 
 // smem of the pipelined chain: BD_NBUF operand pieces + (NSLOT+1)-slot
 // window ring + double-buffered b
+// dev A/B switches (environment, read once per process)
+static int env_flag(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e && e[0] ? atoi(e) : dflt;
+}
+
+// k-split factor of the multi-column chain (k_band_chain_ks); PG_BAND_KS=1
+// selects the single-warp-per-row-tile k_band_chain (A/B measurements)
+static int band_ks() {
+    static const int ks = env_flag("PG_BAND_KS", 2);
+    return ks;
+}
+
 static size_t band_solve_smem(const Level& L, int BC) {
     const int rs = BC == 1 ? 1 : BC + 4;
     if (L.bwin <= 256)          // whole-block TMA ring, 2 NSLOT window ring
@@ -880,9 +902,17 @@ static int launch_dir(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, size_t sm
         CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k<<<grid, BD_CT, sm, st>>>(sa);
     } else {
-        auto k = k_band_chain<BC, CW, NCHK, FWD>;
-        CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k<<<grid, BD_CT, sm, st>>>(sa);
+        const int ks = band_ks();
+        if (ks == 2 || ks == 4) {
+            auto k = ks == 2 ? k_band_chain_ks<BC, CW, NCHK, FWD, 2>
+                             : k_band_chain_ks<BC, CW, NCHK, FWD, 4>;
+            CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k<<<grid, 128 * ks, sm, st>>>(sa);
+        } else {
+            auto k = k_band_chain<BC, CW, NCHK, FWD>;
+            CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k<<<grid, BD_CT, sm, st>>>(sa);
+        }
     }
     LAUNCHED();
     return PG_OK;
@@ -1017,7 +1047,7 @@ static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArg
     int groups = 0;
     for (size_t i = 0; i < hch.size(); ++i) groups += (i == 0 || hch[i].x != hch[i - 1].x);
     if (BCM > 1 && groups <= 2) return spike_fix_gemm(ctx, L, fwd, a, hch, st);
-    const int rows = (L.nblk - (L.spk_P - 1) * L.spk_q) * BD_NB;     // longest (last) chunk
+    const int rows = std::max(L.spk_q, L.nblk - (L.spk_P - 1) * L.spk_q) * BD_NB;  // longest chunk
     dim3 grid((rows + 255) / 256, L.spk_P - 1, nch);
     if (fwd) k_spike_fix<BCM, true><<<grid, 256, sm, st>>>(a);
     else k_spike_fix<BCM, false><<<grid, 256, sm, st>>>(a);
@@ -1164,8 +1194,19 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         CU(cudaMalloc(&L.Y, (size_t)B * L.np * sizeof(double)));
     }
     dim3 gr((L.np + 255) / 256, (B + BD_RHS_CB - 1) / BD_RHS_CB);
-    k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, B, L.row_ptr, L.col_idx, L.m_val, L.n_src,
-                                   L.shapes, u_prev, inv_dt, src, d_perm, L.Y, copy_src);
+    // the scatter (unpartitioned chains) is fused into the k-split backward chain
+    const int ksv = band_ks();
+    const bool fuse = BC >= 8 && L.bwin <= 256 && (ksv == 2 || ksv == 4) &&
+                      env_flag("PG_BAND_FUSE", 1);
+    if (L.dia && !copy_src && L.n_src <= BD_RHS_SRC && L.U <= 4 && env_flag("PG_RHS_DIA", 1)) {
+        RhsDia ra{L.n, L.np, B, L.U, L.n_src, {0, 0, 0, 0, 0}, L.mk, L.shapes};
+        for (int u = 1; u <= L.U; ++u) ra.off[u] = L.off[u];
+        dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
+        k_band_rhs_dia<<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y);
+    } else {
+        k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, B, L.row_ptr, L.col_idx, L.m_val, L.n_src,
+                                       L.shapes, u_prev, inv_dt, src, d_perm, L.Y, copy_src);
+    }
     LAUNCHED();
     const int P = spike ? L.spk_P : 1;
     if (spike) {
@@ -1180,7 +1221,16 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         }
     }
     BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL,
-                     spike ? L.spk_q : L.nblk, P, 0, 0};
+                     spike ? L.spk_q : L.nblk, P, 0, 0, {}};
+    if (fuse && P == 1) {
+        BandSolveArgs::Fuse& f = sa.fz;
+        f.scatter = 1;
+        f.n = L.n;
+        f.perm = d_perm;
+        f.u_out = u_out;
+        f.g = g;
+        f.g_idx = g_idx;
+    }
     const size_t sm = band_solve_smem(L, BC);
     SpikeArgs spa{L.bwin, L.spk_q, P, L.nblk, L.np, B, L.Y, d_chunks, L.d_GF, L.spk_T};
     if ((rc = prof_mark(ctx, 2, st))) return rc;
@@ -1216,6 +1266,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         ctx->ev_used = 0;
         ctx->ev_kind.clear();
     }
+    if (fuse && P == 1) return PG_OK;            // the backward chain wrote u_out
     dim3 gs(std::max(1, std::min(32, (L.n + 255) / 256)), B);
     k_band_scatter<<<gs, 256, 0, st>>>(L.n, L.np, L.Y, d_perm, u_out, g, g_idx);
     LAUNCHED();

@@ -664,6 +664,8 @@ class MgritSolver:
         T = self.transport
         run = SolverRun(n_workers=T.size)
         t_setup = time.perf_counter()
+        self.phi_columns = 0          # per-solve counts (a solver object is reusable)
+        self.phi_calls = 0
         self._initialize_guess()
         if initial_guess is not None:
             self.seed(initial_guess)
