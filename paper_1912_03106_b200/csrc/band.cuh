@@ -859,6 +859,45 @@ k_spike_fix(SpikeArgs a) {
         if (c < ncol) a.Y[(size_t)(col0 + c) * a.ldy + r] += acc[c];
 }
 
+// single-column rank-W update (the coarsest chain's spike correction): the
+// W-term dot product of every row is split over 8 thread slices so a call
+// spreads over (rows / 32) x (P - 1) CTAs instead of a few long serial loops.
+// grid (row tiles of 32, P - 1 chunks, column groups); 256 threads = 32 rows x 8 slices
+template <bool FWD>
+__global__ void __launch_bounds__(256)
+k_spike_fix1(SpikeArgs a) {
+    __shared__ double red[8][33];
+    const int4 ch = a.chunks[blockIdx.z];
+    const double* G = a.G[ch.x];
+    const int col = ch.y;
+    const int p = FWD ? 1 + blockIdx.y : blockIdx.y;    // chunk being fixed
+    const int pb = FWD ? p - 1 : p + 1;                  // chunk holding its border
+    const int r0 = spike_s0(a, p) * BD_NB, r1 = spike_s1(a, p) * BD_NB;
+    const int rl = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const int r = r0 + blockIdx.x * 32 + rl;
+    if (r0 + blockIdx.x * 32 >= r1) return;             // whole tile past the chunk
+    const double* t = a.T + ((size_t)pb * a.ldt + col) * a.W;
+    const int JS = a.W / 8;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (r < r1) {
+        int j = sl * JS;
+        const int je = j + JS;
+        for (; j + 1 < je; j += 2) {
+            acc0 = fma(G[(size_t)j * a.ldy + r], t[j], acc0);
+            acc1 = fma(G[(size_t)(j + 1) * a.ldy + r], t[j + 1], acc1);
+        }
+        if (j < je) acc0 = fma(G[(size_t)j * a.ldy + r], t[j], acc0);
+    }
+    red[sl][rl] = acc0 + acc1;
+    __syncthreads();
+    if (sl == 0 && r < r1) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v += red[q][rl];
+        a.Y[(size_t)col * a.ldy + r] += v;
+    }
+}
+
 // The 512-wide window (511^2 grid; 140 KB of operands per block, two
 // blocks no longer fit in smem).  Warp-specialised pipeline: warp 4 is a TMA
 // producer streaming the block operands piece by piece (D^-1, then CW-column

@@ -1048,6 +1048,13 @@ static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArg
     for (size_t i = 0; i < hch.size(); ++i) groups += (i == 0 || hch[i].x != hch[i - 1].x);
     if (BCM > 1 && groups <= 2) return spike_fix_gemm(ctx, L, fwd, a, hch, st);
     const int rows = std::max(L.spk_q, L.nblk - (L.spk_P - 1) * L.spk_q) * BD_NB;  // longest chunk
+    if (BCM == 1 && L.bwin % 8 == 0) {
+        dim3 g1((rows + 31) / 32, L.spk_P - 1, nch);
+        if (fwd) k_spike_fix1<true><<<g1, 256, 0, st>>>(a);
+        else k_spike_fix1<false><<<g1, 256, 0, st>>>(a);
+        LAUNCHED();
+        return PG_OK;
+    }
     dim3 grid((rows + 255) / 256, L.spk_P - 1, nch);
     if (fwd) k_spike_fix<BCM, true><<<grid, 256, sm, st>>>(a);
     else k_spike_fix<BCM, false><<<grid, 256, sm, st>>>(a);
