@@ -31,6 +31,13 @@ cpu_baseline: the CPU oracle port (oracle/, reference algorithm restated:
          parallel processes), same metric; rank 0 only.
 """
 
+import os as _os
+
+# one BLAS/OpenMP thread per process before numpy loads: the CPU arms run
+# one oracle process per core (no oversubscription in the reference arm)
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    _os.environ.setdefault(_v, "1")
+
 import argparse
 import json
 import os
@@ -308,10 +315,18 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # dev check of the multi-rank plumbing on a 1-GPU box: every rank on
+    # cuda:0, gloo (host-staged) instead of NCCL -- never a measurement
+    share = os.environ.get("PINTGPU_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         transport = DistTransport(device=dev)
     else:
         transport = NullTransport()
