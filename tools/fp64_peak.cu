@@ -42,6 +42,35 @@ __global__ void k_dfma(int iters, double* out) {
     if (s == 1.2345) out[0] = s;
 }
 
+// half the warps issue DMMA, half DFMA: do the two share one fp64 pipe?
+__global__ void k_mixed(int iters, double* out) {
+    const int warp = threadIdx.x >> 5;
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+    double s = 0;
+    if (warp & 1) {
+        double acc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = c;
+        for (int i = 0; i < iters * 8; ++i) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] = fma(a, acc[c], b);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s += acc[c];
+    } else {
+        double acc[8][2];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c][0] = acc[c][1] = 0.0;
+        for (int i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dmma(acc[c][0], acc[c][1], a, b);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s += acc[c][0] + acc[c][1];
+    }
+    if (s == 1.2345) out[0] = s;
+}
+
 int main() {
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -96,6 +125,19 @@ int main() {
         printf(",\n {\"kind\": \"dmma_chains\", \"chains\": %d, \"ns_per_dmma_per_warp\": %.2f,"
                " \"latency_cycles_at_%d_mhz\": %.1f}", chs[ci], per * 1e9, clk / 1000,
                per * chs[ci] * clk * 1e3);
+    }
+    {
+        // mixed: per SM 4 DMMA warps (iters x 8 DMMA) + 4 DFMA warps (8 iters x 8 DFMA)
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0);
+            k_mixed<<<nsm, 256>>>(iters, out);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+        }
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double fl = (double)nsm * 4 * iters * 8 * 512.0 + (double)nsm * 4 * iters * 8 * 8 * 64.0;
+        printf(",\n {\"kind\": \"mixed_dmma_dfma\", \"ms\": %.3f, \"tflops\": %.2f}", ms, fl / ms / 1e9);
     }
     printf("\n]}\n");
     cudaError_t err = cudaGetLastError();
