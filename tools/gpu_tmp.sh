@@ -1,1 +1,1 @@
-mkdir -p gpurun_out; timeout 900 python -m pytest tests/test_gpu_phi.py tests/test_gpu_mgrit.py -x -q > gpurun_out/ab_tests.log 2>&1; timeout 300 python tools/probe_setup.py > gpurun_out/setup.log 2>&1
+mkdir -p gpurun_out; ./tools/mb/rhs_mb > gpurun_out/mb.log 2>&1

@@ -543,6 +543,115 @@ v8(RhsDia a, const double* __restrict__ u_prev, const double* __restrict__ inv_d
 }
 
 
+
+// v13..v16: v1's structure plus, step by step, what the library kernel needs
+template <int STAGE>
+__global__ void __launch_bounds__(256) vs(const double* __restrict__ u, const double* __restrict__ m,
+                                         const int* __restrict__ perm, const double* __restrict__ idt,
+                                         const double* __restrict__ srcv, const double* __restrict__ shp,
+                                         double* __restrict__ Y) {
+    __shared__ int sp[32];
+    __shared__ double sc[32], ss[32][8];
+    if (STAGE >= 1) {
+        for (int t = threadIdx.x; t < 32 * 8; t += 256) {
+            const int j = t / 8, q = t % 8;
+            const int b = perm[blockIdx.y * 32 + j];
+            if (q == 0) { sp[j] = b; sc[j] = idt[b]; }
+            ss[j][q] = q < 6 ? srcv[b * 6 + q] : 0.0;
+        }
+        __syncthreads();
+    }
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= n) return;
+    double mu[4], ml[4];
+    int ou[4], ol[4];
+    for (int k = 0; k < 4; ++k) {
+        const int o = offs[k];
+        mu[k] = i + o < n ? m[k * n + i] : 0.0;
+        ml[k] = (k > 0 && i - o >= 0) ? m[k * n + i - o] : 0.0;
+        ou[k] = i + o < n ? o : 0;
+        ol[k] = i - o >= 0 ? -o : 0;
+    }
+    double sh[8];
+    bool has = false;
+    if (STAGE >= 3) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { sh[q] = q < 6 ? shp[q * n + i] : 0.0; has |= sh[q] != 0.0; }
+    }
+    for (int j = 0; j < 32; ++j) {
+        const int c = blockIdx.y * 32 + j;
+        const int b = STAGE >= 1 ? sp[j] : c;
+        const double* ub = u + (size_t)b * n + i;
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v = fma(mu[k], ub[ou[k]], fma(ml[k], ub[ol[k]], v));
+        if (STAGE == 2) v *= sc[j];
+        if (STAGE == 4) v *= 1.5;
+        if (STAGE == 5) v *= idt[b];
+        if (STAGE >= 3 && has) {
+            double f = 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) f = fma(ss[j][q], sh[q], f);
+            v += f;
+        }
+        Y[(size_t)c * LDY + i] = v;
+    }
+}
+
+// vb<R>: library semantics (perm, c, sources) with R columns' stencil loads
+// issued as one batch before any arithmetic
+template <int R>
+__global__ void __launch_bounds__(256) vb(const double* __restrict__ u, const double* __restrict__ m,
+                                         const int* __restrict__ perm, const double* __restrict__ idt,
+                                         const double* __restrict__ srcv, const double* __restrict__ shp,
+                                         double* __restrict__ Y) {
+    __shared__ int sp[32];
+    __shared__ double sc[32], ss[32][8];
+    for (int t = threadIdx.x; t < 32 * 8; t += 256) {
+        const int j = t / 8, q = t % 8;
+        const int b = perm[blockIdx.y * 32 + j];
+        if (q == 0) { sp[j] = b; sc[j] = idt[b]; }
+        ss[j][q] = q < 6 ? srcv[b * 6 + q] : 0.0;
+    }
+    __syncthreads();
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= n) return;
+    double mv[8];
+    int ov[8];
+    for (int k = 0; k < 4; ++k) {
+        const int o = offs[k];
+        mv[2 * k] = i + o < n ? m[k * n + i] : 0.0;
+        mv[2 * k + 1] = (k > 0 && i - o >= 0) ? m[k * n + i - o] : 0.0;
+        ov[2 * k] = i + o < n ? o : 0;
+        ov[2 * k + 1] = i - o >= 0 ? -o : 0;
+    }
+    double sh[8];
+    bool has = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { sh[q] = q < 6 ? shp[q * n + i] : 0.0; has |= sh[q] != 0.0; }
+    for (int j0 = 0; j0 < 32; j0 += R) {
+        double uv[R][8];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double* ub = u + (size_t)sp[j0 + r] * n + i;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) uv[r][q] = ub[ov[q]];
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int j = j0 + r;
+            double v = mv[0] * uv[r][0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) v = fma(mv[q], uv[r][q], v);
+            double f = 0.0;
+            if (has) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) f = fma(ss[j][q], sh[q], f);
+            }
+            Y[(size_t)(blockIdx.y * 32 + j) * LDY + i] = fma(sc[j], v, f);
+        }
+    }
+}
 int main() {
     double *u, *m, *Y;
     cudaMalloc(&u, (size_t)B * n * 8);
@@ -561,7 +670,7 @@ int main() {
     int* perm; cudaMalloc(&perm, B * 4);
     { std::vector<int> p(B); for (int b = 0; b < B; ++b) p[b] = b; cudaMemcpy(perm, p.data(), B * 4, cudaMemcpyHostToDevice); }
     RhsDia ra{n, LDY, B, 3, 6, {0, 1, NI, NI + 1, 0}, mk, sh};
-    for (int v = 0; v < 13; ++v) {
+    for (int v = 0; v < 22; ++v) {
         float best = 1e9;
         for (int rep = 0; rep < 5; ++rep) {
             cudaEventRecord(e0);
@@ -577,6 +686,15 @@ int main() {
             if (v == 10) v10<<<dim3((LDY + 255) / 256, B / BD_RHS_CC), 256>>>(ra, u, idt, perm, Y);
             if (v == 11) v11<<<dim3((LDY + 255) / 256, B / CC2), 256>>>(ra, u, idt, srcv, perm, Y);
             if (v == 12) v12<NI><<<dim3((LDY + 255) / 256, B / BD_RHS_CC), 256>>>(ra, u, idt, srcv, perm, Y);
+            if (v == 13) vs<1><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
+            if (v == 14) vs<2><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
+            if (v == 15) vs<3><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
+            if (v == 16) vs<0><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
+            if (v == 17) vs<4><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
+            if (v == 18) vs<5><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
+            if (v == 19) vb<1><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
+            if (v == 20) vb<2><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
+            if (v == 21) vb<4><<<dim3((n + 255) / 256, B / 32), 256>>>(u, m, perm, idt, srcv, sh, Y);
             if (v == 5) v5<<<dim3((LDY + 255) / 256, B / BD_RHS_CC), 256>>>(ra, u, idt, perm, Y);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
