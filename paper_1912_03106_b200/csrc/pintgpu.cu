@@ -1044,9 +1044,16 @@ static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArg
     LAUNCHED();
     // one GEMM per factor pays off for few, wide factor groups; many narrow
     // groups (bitwise-distinct dt of one level) go through one fused launch
-    int groups = 0;
-    for (size_t i = 0; i < hch.size(); ++i) groups += (i == 0 || hch[i].x != hch[i - 1].x);
-    if (BCM > 1 && groups <= 2) return spike_fix_gemm(ctx, L, fwd, a, hch, st);
+    // (the fused launch re-reads a factor's G rows once per 8-column chunk: wide
+    // groups -- >= 16 columns per factor on average -- go to the GEMM, which
+    // tiles G once; measured at 512 columns over 9 factors)
+    int groups = 0, cols = 0;
+    for (size_t i = 0; i < hch.size(); ++i) {
+        groups += (i == 0 || hch[i].x != hch[i - 1].x);
+        cols += hch[i].z;
+    }
+    if (BCM > 1 && (groups <= 2 || cols >= 16 * groups))
+        return spike_fix_gemm(ctx, L, fwd, a, hch, st);
     const int rows = std::max(L.spk_q, L.nblk - (L.spk_P - 1) * L.spk_q) * BD_NB;  // longest chunk
     if (BCM == 1 && L.bwin % 8 == 0) {
         dim3 g1((rows + 31) / 32, L.spk_P - 1, nch);
