@@ -65,11 +65,15 @@ struct Level {
     };
     std::unordered_map<uint64_t, std::vector<Group>> groups;
     Group tmp_group{};
-    // SPIKE partition of the chains for latency-bound batches (B <= #SMs)
-    int spk_q = 0, spk_P = 1;
-    std::vector<double*> GF, GB;            // per factor: [W][np] spikes (lazy)
-    double** d_GF = nullptr;
-    double** d_GB = nullptr;
+    // SPIKE partitions of the chains for latency-bound batches: ~8, 4 and 2
+    // chunks (a call takes the finest one whose column groups x chunks still
+    // fit the SMs); each has its own per-factor spikes, computed lazily
+    struct SpikePart {
+        int q = 0, P = 1;
+        std::vector<double*> GF, GB;        // per factor: [W][np] spikes
+        double** d_GF = nullptr;
+        double** d_GB = nullptr;
+    } spk[3];
     double* spk_T = nullptr;                // [P][W][B] border values
     size_t spk_T_cap = 0;
     int4* d_spk_chunks = nullptr;           // spike generation column groups
@@ -224,16 +228,19 @@ static void free_level(Level& L) {
     void* ptrs[] = {L.row_ptr, L.col_idx, L.m_val, L.k_val, L.dM, L.dK, L.shapes,
                     L.weights, L.tile_lo, L.tile_hi, L.elem_dof, L.elem_geo,
                     L.ne_ptr, L.ne, L.mk, L.d_FL, L.d_FU, L.Y, L.d_perm,
-                    L.d_chunks, L.d_status, L.k_pre, L.d_GF, L.d_GB, L.spk_T,
-                    L.d_spk_chunks};
+                    L.d_chunks, L.d_status, L.k_pre, L.spk_T, L.d_spk_chunks};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : L.ws_allocs) cudaFree(p);
     L.ws_allocs.clear();
     for (double* p : L.FL) cudaFree(p);
     for (double* p : L.FU) cudaFree(p);
-    for (double* p : L.GF) if (p) cudaFree(p);
-    for (double* p : L.GB) if (p) cudaFree(p);
+    for (auto& sp : L.spk) {
+        for (double* p : sp.GF) if (p) cudaFree(p);
+        for (double* p : sp.GB) if (p) cudaFree(p);
+        if (sp.d_GF) cudaFree(sp.d_GF);
+        if (sp.d_GB) cudaFree(sp.d_GB);
+    }
     for (auto& kv : L.groups)
         for (auto& gr : kv.second) { cudaFree(gr.perm); cudaFree(gr.chunks); }
     L.groups.clear();
@@ -319,17 +326,20 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
     L.nblk = (d->n + BD_NB - 1) / BD_NB;
     L.np = L.nblk * BD_NB;
     L.band_ok = L.bwin <= 512;
-    // SPIKE chunks: ~8 chunks of >= max(NSLOT, 8) blocks
-    {
+    // SPIKE chunks: ~8 / 4 / 2 chunks of >= max(NSLOT, 8) blocks (8 measured
+    // best on config 2's 64-column calls, against 4, 6, 12, 16, 24 and 32)
+    for (int pi = 0; pi < 3; ++pi) {
         const int nslot = L.bwin / BD_NB;
-        int target = 8;          // measured on config 2: 8 chunks beat 4, 6, 12, 16, 24, 32
-        if (const char* e = getenv("PG_SPIKE_CHUNKS")) target = std::max(2, atoi(e));  // dev A/B
-        L.spk_q = std::max((L.nblk + target - 1) / target, std::max(nslot, 8));
+        int target = 8 >> pi;
+        if (const char* e = getenv("PG_SPIKE_CHUNKS"))               // dev A/B
+            target = std::max(2, atoi(e) >> pi);
+        Level::SpikePart& sp = L.spk[pi];
+        sp.q = std::max((L.nblk + target - 1) / target, std::max(nslot, 8));
         // balanced: ceil, with the remainder as a shorter last chunk (it still
         // holds >= NSLOT blocks: its head is the border of the chunk before)
-        L.spk_P = (L.nblk + L.spk_q - 1) / L.spk_q;
-        if (L.nblk - (L.spk_P - 1) * L.spk_q < nslot) --L.spk_P;
-        if (L.spk_P < 2) L.spk_P = 1;
+        sp.P = (L.nblk + sp.q - 1) / sp.q;
+        if (L.nblk - (sp.P - 1) * sp.q < nslot) --sp.P;
+        if (sp.P < 2) sp.P = 1;
     }
     // rows per tile: 1024 (4 rows per thread); halo from the CSR
     L.R = 1024;
@@ -839,21 +849,27 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
         L.FU.push_back(fu);
     }
     const int total = (int)L.FL.size();
-    L.GF.resize(total, nullptr);
-    L.GB.resize(total, nullptr);
+    for (auto& sp : L.spk) {
+        sp.GF.resize(total, nullptr);
+        sp.GB.resize(total, nullptr);
+    }
     if (total > L.fac_cap) {
         if (L.d_FL) cudaFree(L.d_FL);
         if (L.d_FU) cudaFree(L.d_FU);
-        if (L.d_GF) cudaFree(L.d_GF);
-        if (L.d_GB) cudaFree(L.d_GB);
         L.fac_cap = std::max(64, 2 * total);
         CU(cudaMalloc(&L.d_FL, L.fac_cap * sizeof(double*)));
         CU(cudaMalloc(&L.d_FU, L.fac_cap * sizeof(double*)));
-        CU(cudaMalloc(&L.d_GF, L.fac_cap * sizeof(double*)));
-        CU(cudaMalloc(&L.d_GB, L.fac_cap * sizeof(double*)));
+        for (auto& sp : L.spk) {
+            if (sp.d_GF) cudaFree(sp.d_GF);
+            if (sp.d_GB) cudaFree(sp.d_GB);
+            CU(cudaMalloc(&sp.d_GF, L.fac_cap * sizeof(double*)));
+            CU(cudaMalloc(&sp.d_GB, L.fac_cap * sizeof(double*)));
+        }
     }
-    CU(cudaMemcpyAsync(L.d_GF, L.GF.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(L.d_GB, L.GB.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
+    for (auto& sp : L.spk) {
+        CU(cudaMemcpyAsync(sp.d_GF, sp.GF.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(sp.d_GB, sp.GB.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
+    }
     CU(cudaMemcpyAsync(L.d_FL, L.FL.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(L.d_FU, L.FU.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
     if (!L.d_status) CU(cudaMalloc(&L.d_status, sizeof(int)));
@@ -946,15 +962,16 @@ static int band_dir(pg_ctx* ctx, const Level& L, int BC, bool fwd, const BandSol
 
 // spikes of factor f (response of every chunk's chain to unit border values),
 // computed once per factor by the 8-column chain in spike mode
-static int ensure_spikes(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
-    if (L.GF[f]) return PG_OK;
+static int ensure_spikes(pg_ctx* ctx, Level& L, int pi, int f, cudaStream_t st) {
+    Level::SpikePart& sp = L.spk[pi];
+    if (sp.GF[f]) return PG_OK;
     const size_t bytes = (size_t)L.bwin * L.np * sizeof(double);
-    CU(cudaMalloc(&L.GF[f], bytes));
-    CU(cudaMalloc(&L.GB[f], bytes));
-    CU(cudaMemsetAsync(L.GF[f], 0, bytes, st));
-    CU(cudaMemsetAsync(L.GB[f], 0, bytes, st));
-    CU(cudaMemcpyAsync(L.d_GF + f, &L.GF[f], sizeof(double*), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(L.d_GB + f, &L.GB[f], sizeof(double*), cudaMemcpyHostToDevice, st));
+    CU(cudaMalloc(&sp.GF[f], bytes));
+    CU(cudaMalloc(&sp.GB[f], bytes));
+    CU(cudaMemsetAsync(sp.GF[f], 0, bytes, st));
+    CU(cudaMemsetAsync(sp.GB[f], 0, bytes, st));
+    CU(cudaMemcpyAsync(sp.d_GF + f, &sp.GF[f], sizeof(double*), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(sp.d_GB + f, &sp.GB[f], sizeof(double*), cudaMemcpyHostToDevice, st));
     const int ng = L.bwin / 8;
     if (!L.d_spk_chunks) CU(cudaMalloc(&L.d_spk_chunks, 64 * sizeof(int4)));   // W <= 512
     std::vector<int4> ch(ng);
@@ -962,19 +979,19 @@ static int ensure_spikes(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
     CU(cudaMemcpyAsync(L.d_spk_chunks, ch.data(), ng * sizeof(int4), cudaMemcpyHostToDevice, st));
     CU(cudaStreamSynchronize(st));               // ch leaves scope
     const size_t sm = band_solve_smem(L, 8);
-    BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.GF[f], L.d_spk_chunks, L.d_FL,
-                     L.spk_q, L.spk_P, 1, 1};
+    BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, sp.GF[f], L.d_spk_chunks, L.d_FL,
+                     sp.q, sp.P, 1, 1};
     int rc;
-    if ((rc = band_dir(ctx, L, 8, true, sa, dim3(ng, L.spk_P - 1), sm, st))) return rc;
-    sa.Y = L.GB[f];
+    if ((rc = band_dir(ctx, L, 8, true, sa, dim3(ng, sp.P - 1), sm, st))) return rc;
+    sa.Y = sp.GB[f];
     sa.F = L.d_FU;
     sa.p0 = 0;
-    return band_dir(ctx, L, 8, false, sa, dim3(ng, L.spk_P - 1), sm, st);
+    return band_dir(ctx, L, 8, false, sa, dim3(ng, sp.P - 1), sm, st);
 }
 
 // y_p += G_p t_{p-1 / p+1} for every non-first chunk: a plain rank-W GEMM per
 // factor (columns [c0, c1) of the grouped batch), cuBLAS DGEMM (fp64 DMMA)
-static int spike_fix_gemm(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArgs& a,
+static int spike_fix_gemm(pg_ctx* ctx, const Level::SpikePart& sp, bool fwd, const SpikeArgs& a,
                           const std::vector<int4>& hch, cudaStream_t st) {
     if (!ctx->cublas && cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS)
         return set_err(ctx, PG_ECUDA, "cublasCreate failed");
@@ -984,7 +1001,7 @@ static int spike_fix_gemm(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArgs
     const int W = a.W, P = a.P, ru = a.q * BD_NB;
     const int rl = (a.nblk - (P - 1) * a.q) * BD_NB;         // last (longest) chunk
     const long long sT = (long long)a.ldt * W;
-    const std::vector<double*>& G = fwd ? L.GF : L.GB;
+    const std::vector<double*>& G = fwd ? sp.GF : sp.GB;
     for (size_t i = 0; i < hch.size();) {
         size_t j = i;
         while (j < hch.size() && hch[j].x == hch[i].x) ++j;
@@ -1018,7 +1035,8 @@ static int spike_fix_gemm(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArgs
 }
 
 template <int BCM>
-static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArgs& a, int nch,
+static int spike_recombine(pg_ctx* ctx, const Level& L, const Level::SpikePart& sp, bool fwd,
+                           const SpikeArgs& a, int nch,
                            const std::vector<int4>& hch, cudaStream_t st) {
     const size_t sm = (size_t)L.bwin * BCM * sizeof(double);
     const size_t smb = sm + (size_t)1024 * BCM * sizeof(double);   // + red[S][BCM][W]
@@ -1045,24 +1063,24 @@ static int spike_recombine(pg_ctx* ctx, const Level& L, bool fwd, const SpikeArg
     // one GEMM per factor pays off for few, wide factor groups; many narrow
     // groups (bitwise-distinct dt of one level) go through one fused launch
     // (the fused launch re-reads a factor's G rows once per 8-column chunk: wide
-    // groups -- >= 16 columns per factor on average -- go to the GEMM, which
-    // tiles G once; measured at 512 columns over 9 factors)
+    // groups -- >= 48 columns per factor on average -- go to the GEMMs, which
+    // tile G once; narrower ones are not worth ~2 small GEMM launches per factor)
     int groups = 0, cols = 0;
     for (size_t i = 0; i < hch.size(); ++i) {
         groups += (i == 0 || hch[i].x != hch[i - 1].x);
         cols += hch[i].z;
     }
-    if (BCM > 1 && (groups <= 2 || cols >= 16 * groups))
-        return spike_fix_gemm(ctx, L, fwd, a, hch, st);
-    const int rows = std::max(L.spk_q, L.nblk - (L.spk_P - 1) * L.spk_q) * BD_NB;  // longest chunk
+    if (BCM > 1 && (groups <= 2 || cols >= 48 * groups))
+        return spike_fix_gemm(ctx, sp, fwd, a, hch, st);
+    const int rows = std::max(a.q, a.nblk - (a.P - 1) * a.q) * BD_NB;  // longest chunk
     if (BCM == 1 && L.bwin % 8 == 0) {
-        dim3 g1((rows + 31) / 32, L.spk_P - 1, nch);
+        dim3 g1((rows + 31) / 32, a.P - 1, nch);
         if (fwd) k_spike_fix1<true><<<g1, 256, 0, st>>>(a);
         else k_spike_fix1<false><<<g1, 256, 0, st>>>(a);
         LAUNCHED();
         return PG_OK;
     }
-    dim3 grid((rows + 255) / 256, L.spk_P - 1, nch);
+    dim3 grid((rows + 255) / 256, a.P - 1, nch);
     if (fwd) k_spike_fix<BCM, true><<<grid, 256, sm, st>>>(a);
     else k_spike_fix<BCM, false><<<grid, 256, sm, st>>>(a);
     LAUNCHED();
@@ -1143,10 +1161,10 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         CU(cudaMemcpyAsync(c.data(), inv_dt, B * sizeof(double), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
     }
-    // latency-bound batches run the SPIKE-partitioned chains
-    // (up to ~n_sm/2 column groups of 8: below that the GPU is underfilled)
-    const bool spike = L.spk_P > 1 && B <= 4 * ctx->n_sm;
-    const int BC = spike ? (B >= 16 ? 8 : 1) : band_solve_bc(L, B, ctx->n_sm);
+    // latency-bound batches (column groups well below the SM count) run the
+    // SPIKE-partitioned chains; the partition is picked after the grouping
+    const bool spike_ok = L.spk[0].P > 1 && B <= 4 * ctx->n_sm;
+    const int BC = spike_ok ? (B >= 16 ? 8 : 1) : band_solve_bc(L, B, ctx->n_sm);
     // cached grouping for this exact inv_dt pattern?
     const uint64_t h = hash_doubles(c.data(), B);
     Level::Group* grp = nullptr;
@@ -1222,11 +1240,19 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
                                        L.shapes, u_prev, inv_dt, src, d_perm, L.Y, copy_src);
     }
     LAUNCHED();
-    const int P = spike ? L.spk_P : 1;
+    // finest partition (8, 4, 2 chunks) whose chunk CTAs fit one wave; none:
+    // the plain chains (the column groups already cover the SMs)
+    int pi = -1;
+    for (int t = 0; spike_ok && t < 3 && pi < 0; ++t)
+        if (L.spk[t].P > 1 && nch * L.spk[t].P <= ctx->n_sm) pi = t;
+    if (spike_ok && pi < 0 && nch <= ctx->n_sm / 2) pi = 2;   // 2 chunks still halve the chain
+    const bool spike = pi >= 0;
+    const Level::SpikePart& spp = L.spk[spike ? pi : 0];
+    const int P = spike ? spp.P : 1;
     if (spike) {
         // factors of this call (host copy of the chunks: no device round trip)
         for (const int4& q : grp->hch)
-            if (!L.GF[q.x] && (rc = ensure_spikes(ctx, L, q.x, st))) return rc;
+            if (!spp.GF[q.x] && (rc = ensure_spikes(ctx, L, pi, q.x, st))) return rc;
         const size_t tneed = (size_t)P * L.bwin * B;
         if (tneed > L.spk_T_cap) {
             if (L.spk_T) cudaFree(L.spk_T);
@@ -1235,7 +1261,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         }
     }
     BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL,
-                     spike ? L.spk_q : L.nblk, P, 0, 0, {}};
+                     spike ? spp.q : L.nblk, P, 0, 0, {}};
     if (fuse && P == 1) {
         BandSolveArgs::Fuse& f = sa.fz;
         f.scatter = 1;
@@ -1246,16 +1272,16 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         f.g_idx = g_idx;
     }
     const size_t sm = band_solve_smem(L, BC);
-    SpikeArgs spa{L.bwin, L.spk_q, P, L.nblk, L.np, B, L.Y, d_chunks, L.d_GF, L.spk_T};
+    SpikeArgs spa{L.bwin, spp.q, P, L.nblk, L.np, B, L.Y, d_chunks, spp.d_GF, L.spk_T};
     if ((rc = prof_mark(ctx, 2, st))) return rc;
     for (int dir = 0; dir < 2 && !rc; ++dir) {
         const bool fwd = dir == 0;
         sa.F = fwd ? L.d_FL : L.d_FU;
         if ((rc = band_dir(ctx, L, BC, fwd, sa, dim3(nch, P), sm, st))) break;
         if (spike) {
-            spa.G = fwd ? L.d_GF : L.d_GB;
-            rc = BC == 1 ? spike_recombine<1>(ctx, L, fwd, spa, nch, grp->hch, st)
-                         : spike_recombine<8>(ctx, L, fwd, spa, nch, grp->hch, st);
+            spa.G = fwd ? spp.d_GF : spp.d_GB;
+            rc = BC == 1 ? spike_recombine<1>(ctx, L, spp, fwd, spa, nch, grp->hch, st)
+                         : spike_recombine<8>(ctx, L, spp, fwd, spa, nch, grp->hch, st);
         }
     }
     if (rc) return rc;
