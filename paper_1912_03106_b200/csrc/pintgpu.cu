@@ -11,6 +11,7 @@
 #include "newton_nk.cuh"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -841,6 +842,12 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     if (!nf) return PG_OK;
     const int first = (int)L.FL.size();
     const size_t fbytes = (size_t)L.nblk * bd_block_doubles(L.bwin) * sizeof(double);
+    static const int dbg = env_flag("PG_DEBUG_SETUP", 0);
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t0 = now();
     for (int f = 0; f < nf; ++f) {
         double *fl = nullptr, *fu = nullptr;
         CU(cudaMalloc(&fl, fbytes));
@@ -877,11 +884,14 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     // scratch lower bands
     std::vector<double*> lbs(nf);
     const size_t lbytes = (size_t)L.n * (L.bw + 1) * sizeof(double);
-    for (int f = 0; f < nf; ++f) CU(cudaMallocAsync(&lbs[f], lbytes, st));
+    for (int f = 0; f < nf; ++f) CU(cudaMalloc(&lbs[f], lbytes));
     double** d_lb;
     double* d_c;
-    CU(cudaMallocAsync(&d_lb, nf * sizeof(double*), st));
-    CU(cudaMallocAsync(&d_c, nf * sizeof(double), st));
+    // plain allocations, freed after the status sync below: the stream-ordered
+    // pool grew (and re-mapped) ~0.5 GB of scratch per call, which cost up to
+    // 0.4 s on a box with another problem resident (measured)
+    CU(cudaMalloc(&d_lb, nf * sizeof(double*)));
+    CU(cudaMalloc(&d_c, nf * sizeof(double)));
     CU(cudaMemcpyAsync(d_lb, lbs.data(), nf * sizeof(double*), cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_c, cs.data(), nf * sizeof(double), cudaMemcpyHostToDevice, st));
     BandFactorArgs a{L.n, L.bw, L.bwin, L.LDA, L.nblk, L.row_ptr, L.col_idx, L.m_val,
@@ -894,12 +904,17 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     CU(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_band_factor<<<nf, 256, sm, st>>>(a, d_lb, L.d_FL + first, L.d_FU + first, L.d_status);
     LAUNCHED();
-    for (int f = 0; f < nf; ++f) CU(cudaFreeAsync(lbs[f], st));
-    CU(cudaFreeAsync(d_lb, st));
-    CU(cudaFreeAsync(d_c, st));
+
+    const auto t1 = now();
     int status = 0;
     CU(cudaMemcpyAsync(&status, L.d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    for (int f = 0; f < nf; ++f) cudaFree(lbs[f]);    // after the sync: no implicit wait
+    cudaFree(d_lb);
+    cudaFree(d_c);
+    if (dbg)
+        fprintf(stderr, "[pintgpu] band_factors n=%d nf=%d: host %.2f ms, kernels+sync %.2f ms\n",
+                L.n, nf, ms(t0, t1), ms(t1, now()));
     if (status)
         return set_err(ctx, PG_EINVAL, "matrix not positive definite (pivot %d)", status - 1);
     return PG_OK;

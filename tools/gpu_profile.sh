@@ -1,6 +1,6 @@
-# round profile refresh: bench line, reference arm, launch list, full capture of the top kernel
+# round profile refresh: bench line, reference arm, launch list
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 34000 --launch-count 11000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-phi --no-seq > gpurun_out/ncu.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_band_chain_ks -s 2 -c 2 -o gpurun_out/chain_full python tools/probe_band.py cfg2 0:1024 > gpurun_out/ncu_full.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_phi.py tests/test_gpu_mgrit.py -x -q > gpurun_out/ab_tests.log 2>&1
-timeout 600 python tools/probe_scaling.py > gpurun_out/scal.log 2>&1
-timeout 300 python tools/probe_breakdown.py cfg2 >> gpurun_out/scal.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab_tests.log 2>&1
+timeout 900 python bench.py --no-cpu > gpurun_out/bench.json 2> gpurun_out/bench.err
