@@ -881,12 +881,22 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     CU(cudaMemcpyAsync(L.d_FU, L.FU.data(), total * sizeof(double*), cudaMemcpyHostToDevice, st));
     if (!L.d_status) CU(cudaMalloc(&L.d_status, sizeof(int)));
     CU(cudaMemsetAsync(L.d_status, 0, sizeof(int), st));
-    // scratch lower bands
-    std::vector<double*> lbs(nf);
+    // scratch lower bands (freed on every exit path, including CU errors)
+    std::vector<double*> lbs(nf, nullptr);
+    double** d_lb = nullptr;
+    double* d_c = nullptr;
+    struct Scratch {
+        std::vector<double*>& lbs;
+        double**& d_lb;
+        double*& d_c;
+        ~Scratch() {
+            for (double* p : lbs) if (p) cudaFree(p);
+            if (d_lb) cudaFree(d_lb);
+            if (d_c) cudaFree(d_c);
+        }
+    } scratch{lbs, d_lb, d_c};
     const size_t lbytes = (size_t)L.n * (L.bw + 1) * sizeof(double);
     for (int f = 0; f < nf; ++f) CU(cudaMalloc(&lbs[f], lbytes));
-    double** d_lb;
-    double* d_c;
     // plain allocations, freed after the status sync below: the stream-ordered
     // pool grew (and re-mapped) ~0.5 GB of scratch per call, which cost up to
     // 0.4 s on a box with another problem resident (measured)
@@ -909,9 +919,7 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     int status = 0;
     CU(cudaMemcpyAsync(&status, L.d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    for (int f = 0; f < nf; ++f) cudaFree(lbs[f]);    // after the sync: no implicit wait
-    cudaFree(d_lb);
-    cudaFree(d_c);
+    // (scratch freed by the guard after the sync: cudaFree then waits on nothing)
     if (dbg)
         fprintf(stderr, "[pintgpu] band_factors n=%d nf=%d: host %.2f ms, kernels+sync %.2f ms\n",
                 L.n, nf, ms(t0, t1), ms(t1, now()));
