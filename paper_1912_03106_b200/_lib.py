@@ -10,8 +10,9 @@ import os
 
 from .errors import NewtonConvergenceError, PintGpuError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
-                        "libpintgpu.so")
+# PINTGPU_LIB: dev override for A/B builds of the library
+LIB_PATH = os.environ.get("PINTGPU_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libpintgpu.so")
 
 PG_OK, PG_EINVAL, PG_ECUDA, PG_ENEWTON, PG_ENOCONV = 0, 1, 2, 3, 4
 PG_INNER_PCG, PG_INNER_CHOLESKY = 0, 1
