@@ -383,35 +383,45 @@ def run_b200(args):
     # --- end to end through the public API: host spec in (assembly + H2D of
     # the level data and excitation tables, factorisation), solve, D2H of the
     # solution at the C-points (the MGRIT iterate) into pinned host memory
+    # Run E2E_REPS times (each a fresh problem and solver); the median is
+    # reported, every repetition is listed (the setup's allocations vary by
+    # box and by what else is resident).
     lvl0 = solver.levels[0]
     host = torch.empty((lvl0.K, lvl0.n), dtype=torch.float64, pin_memory=True)
-    barrier()
-    t0 = time.perf_counter()
-    p2 = GpuFemProblem(spec, device=local)
-    h2d = sum(g.row_ptr.nbytes + g.col_idx.nbytes + g.m_val.nbytes + g.k_val.nbytes
-              + g.shapes.nbytes + g.weights.nbytes for g in p2.grids)
-    torch.cuda.synchronize(dev)
-    t1 = time.perf_counter()
-    s2, _ = make_solver(p2)                 # includes the banded factorisations
-    h2d += sum(lv.inv_dt_all.numel() * 8 + sum(t.numel() * 8 for t in lv.src_all)
-               for lv in s2.levels)
-    torch.cuda.synchronize(dev)
-    t2 = time.perf_counter()
-    run2, _ = s2.solve(gather_solution=False)
-    torch.cuda.synchronize(dev)
-    t3 = time.perf_counter()
-    host.copy_(s2.levels[0].c_store, non_blocking=True)
-    barrier()
-    e2e_s = time.perf_counter() - t0
-    e2e_parts = {"problem_s": t1 - t0, "solver_setup_s": t2 - t1, "solve_s": t3 - t2,
+    e2e_runs = []
+    for _ in range(max(1, args.e2e_reps)):
+        barrier()
+        t0 = time.perf_counter()
+        p2 = GpuFemProblem(spec, device=local)
+        h2d = sum(g.row_ptr.nbytes + g.col_idx.nbytes + g.m_val.nbytes + g.k_val.nbytes
+                  + g.shapes.nbytes + g.weights.nbytes for g in p2.grids)
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        s2, _ = make_solver(p2)                 # includes the banded factorisations
+        h2d += sum(lv.inv_dt_all.numel() * 8 + sum(t.numel() * 8 for t in lv.src_all)
+                   for lv in s2.levels)
+        torch.cuda.synchronize(dev)
+        t2 = time.perf_counter()
+        run2, _ = s2.solve(gather_solution=False)
+        torch.cuda.synchronize(dev)
+        t3 = time.perf_counter()
+        host.copy_(s2.levels[0].c_store, non_blocking=True)
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        parts = {"problem_s": t1 - t0, "solver_setup_s": t2 - t1, "solve_s": t3 - t2,
                  "d2h_s": e2e_s - (t3 - t0)}
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e_runs.append((e2e_s, parts))
+        del s2
+        p2.close()
+    e2e_sorted = sorted(e2e_runs, key=lambda x: x[0])
+    e2e_s, e2e_parts = e2e_sorted[len(e2e_sorted) // 2]
+    e2e_all = [round(x[0], 4) for x in e2e_runs]
     d2h = int(host.numel() * 8)
     del host
-    p2.close()
 
     # --- GPU sequential time stepping (the time-to-solution baseline)
     seq_s = None
@@ -475,7 +485,8 @@ def run_b200(args):
                   "phi_columns_per_solve": r.phi_columns, "phi_calls_per_solve": r.phi_calls},
         "e2e": {"value": n_steps * n0 / e2e_s, "unit": "fine time-step*DOF/s",
                 "seconds": e2e_s, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h,
-                "parts": e2e_parts},
+                "parts": e2e_parts, "reps_s": e2e_all,
+                "stat": "median of the repetitions in reps_s"},
         "roofline": roofline,
         "phi_microbench": phi_bench,
         "cpu_baseline": cpu,
@@ -496,6 +507,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-phi", action="store_true", help="skip the config-5 batched-Phi leg")
+    ap.add_argument("--e2e-reps", type=int, default=3,
+                    help="end-to-end repetitions (median reported)")
     ap.add_argument("--no-seq", action="store_true", help="skip the GPU sequential-stepping leg")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -344,6 +344,8 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
     }
     // rows per tile: 1024 (4 rows per thread); halo from the CSR
     L.R = 1024;
+    if (const char* e = getenv("PG_TILE_R"))                         // dev A/B
+        L.R = std::max(256, atoi(e) & ~1);
     L.n_tiles = (d->n + L.R - 1) / L.R;
     std::vector<int> lo(L.n_tiles), hi(L.n_tiles);
     L.span_max = 0;
@@ -421,7 +423,9 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
                 L.ld = (d->n + 31) & ~31;
                 const int span = L.R + 2 * L.omax + 4;
                 L.Cd = 4;                 // 2 halo arrays per column, <= 72 KB / CTA
-                while (L.Cd > 1 && (size_t)L.Cd * 2 * span * 8 > 72 * 1024) L.Cd >>= 1;
+                size_t cap = 72 * 1024;
+                if (const char* e = getenv("PG_DIA_CTA_KB")) cap = (size_t)atoi(e) * 1024;  // dev A/B
+                while (L.Cd > 1 && (size_t)L.Cd * 2 * span * 8 > cap) L.Cd >>= 1;
                 if ((size_t)span * 8 > 200 * 1024 || U == 0) L.dia = false;
                 if (L.dia) {
                     int rc0 = dev_upload(ctx, &L.mk, mk.data(), mk.size());
@@ -665,9 +669,9 @@ static int launch_dia_iter_c(pg_ctx* ctx, Level& L, int na, int cur, const doubl
                                 200 * 1024));
         attr_done = true;
     }
-    dim3 gd(L.n_tiles, (na + C - 1) / C);
     int rc;
     if ((rc = prof_mark(ctx, 0, st))) return rc;
+    dim3 gd(L.n_tiles, (na + C - 1) / C);
     k_sdir<C, UU><<<gd, PG_DIA_NT, sm, st>>>(dia_view(L), L.V, L.W, L.qv, cur, inv_dt, SPAN);
     LAUNCHED();
     if ((rc = prof_mark(ctx, 0, st))) return rc;
@@ -1256,8 +1260,20 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     if (L.dia && !copy_src && L.n_src <= BD_RHS_SRC && L.U <= 4 && env_flag("PG_RHS_DIA", 1)) {
         RhsDia ra{L.n, L.np, B, L.U, L.n_src, {0, 0, 0, 0, 0}, L.mk, L.shapes};
         for (int u = 1; u <= L.U; ++u) ra.off[u] = L.off[u];
-        dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
-        k_band_rhs_dia<<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y);
+        static const int rhs_sm = env_flag("PG_RHS_SM", 0);       // dev A/B
+        const int ldh = (256 + 2 * L.omax + 255) / 256;        // halo loads per thread
+        if (rhs_sm && ldh <= 4) {
+            dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
+            const size_t smr = (size_t)2 * (256 + 2 * L.omax) * sizeof(double);
+            switch (ldh) {
+                case 1: case 2: k_band_rhs_sm<1, 2><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
+                case 3: k_band_rhs_sm<1, 3><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
+                default: k_band_rhs_sm<1, 4><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
+            }
+        } else {
+            dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
+            k_band_rhs_dia<<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y);
+        }
     } else {
         k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, B, L.row_ptr, L.col_idx, L.m_val, L.n_src,
                                        L.shapes, u_prev, inv_dt, src, d_perm, L.Y, copy_src);
