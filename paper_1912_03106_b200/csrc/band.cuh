@@ -1360,6 +1360,110 @@ k_band_rhs_sm(RhsDia a, const double* __restrict__ u_prev, const double* __restr
     }
 }
 
+// Same rhs, S-stage cp.async ring: the halos of the next S - 1 columns are in
+// flight (LDGSTS, zero-filled outside [0, n)) while column j is computed from
+// shared memory -- bytes in flight per CTA no longer depend on registers.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int S, int LD>
+__global__ void __launch_bounds__(256)
+k_band_rhs_cp(RhsDia a, const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
+              const double* __restrict__ src, const int* __restrict__ perm,
+              double* __restrict__ Y) {
+    extern __shared__ double su[];           // [S][span]
+    __shared__ int sp[BD_RHS_CC];
+    __shared__ double sc[BD_RHS_CC], ss[BD_RHS_CC][BD_RHS_SRC];
+    const int gc0 = blockIdx.y * BD_RHS_CC;
+    const int ncol = min(BD_RHS_CC, a.B - gc0);
+    for (int t = threadIdx.x; t < BD_RHS_CC * BD_RHS_SRC; t += blockDim.x) {
+        const int j = t / BD_RHS_SRC, q = t % BD_RHS_SRC;
+        const int b = j < ncol ? perm[gc0 + j] : 0;
+        if (q == 0) {
+            sp[j] = b;
+            sc[j] = j < ncol ? inv_dt[b] : 0.0;
+        }
+        ss[j][q] = (j < ncol && q < a.n_src) ? src[(size_t)b * a.n_src + q] : 0.0;
+    }
+    const int omax = a.off[a.U];
+    const int r0 = blockIdx.x * 256;
+    const int lo = r0 - omax;
+    const int span = 256 + 2 * omax;
+    const int i = r0 + threadIdx.x;
+    const int ic = min(i, a.n - 1);
+    double m0, mup[4], mlo[4], sh[BD_RHS_SRC];
+    int oup[4], olo[4];
+    m0 = a.mk[ic].x;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int o = a.off[u + 1];
+        const bool on = u < a.U;
+        const bool hu = on && ic + o < a.n, hl = on && ic - o >= 0;
+        mup[u] = hu ? a.mk[(size_t)(u + 1) * a.n + ic].x : 0.0;
+        mlo[u] = hl ? a.mk[(size_t)(u + 1) * a.n + ic - o].x : 0.0;
+        oup[u] = hu ? o : 0;
+        olo[u] = hl ? -o : 0;
+    }
+    bool has_src = false;
+#pragma unroll
+    for (int q = 0; q < BD_RHS_SRC; ++q) {
+        sh[q] = q < a.n_src ? a.shapes[(size_t)q * a.n + ic] : 0.0;
+        has_src |= sh[q] != 0.0;
+    }
+    __syncthreads();
+    auto issue = [&](int j) {
+        const double* ub = u_prev + (size_t)sp[j] * a.n;
+        double* s = su + (size_t)(j % S) * span;
+#pragma unroll
+        for (int t = 0; t < LD; ++t) {
+            const int jj = threadIdx.x + 256 * t;
+            if (jj < span) {
+                const int g = lo + jj;
+                const bool ok = g >= 0 && g < a.n;
+                cp_async8(s + jj, ok ? ub + g : ub, ok ? 8 : 0);
+            }
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j) {
+        if (j < ncol) issue(j);
+        cp_async_commit();
+    }
+    for (int j = 0; j < ncol; ++j) {
+        cp_async_wait<S - 2>();
+        __syncthreads();                 // column j landed; slot (j - 1) % S is free
+        if (j + S - 1 < ncol) issue(j + S - 1);
+        cp_async_commit();
+        if (i < a.ldy) {
+            double* yo = Y + (size_t)(gc0 + j) * a.ldy + i;
+            if (i >= a.n) {
+                *yo = 0.0;
+            } else {
+                const double* ub = su + (size_t)(j % S) * span + (i - lo);
+                double v = m0 * ub[0];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v = fma(mup[u], ub[oup[u]], fma(mlo[u], ub[olo[u]], v));
+                double f = 0.0;
+                if (has_src) {
+#pragma unroll
+                    for (int q = 0; q < BD_RHS_SRC; ++q) f = fma(ss[j][q], sh[q], f);
+                }
+                *yo = fma(sc[j], v, f);
+            }
+        }
+    }
+}
+
 // u_out[perm[gc]] = Y[gc] (+ g)
 __global__ void k_band_scatter(int n, int ldy, const double* __restrict__ Y,
                                const int* __restrict__ perm, double* __restrict__ u_out,

@@ -50,7 +50,8 @@ struct Level {
     bool band_ok = false;
     std::unordered_map<uint64_t, int> fac_index;
     std::vector<double> fac_c;             // 1/dt of every factor (index = factor id)
-    std::vector<double*> FL, FU;
+    std::vector<double*> FL, FU;            // views into fac_slabs
+    std::vector<void*> fac_slabs;           // one allocation per band_factors call
     double** d_FL = nullptr;
     double** d_FU = nullptr;
     int fac_cap = 0;
@@ -234,8 +235,10 @@ static void free_level(Level& L) {
         if (p) cudaFree(p);
     for (void* p : L.ws_allocs) cudaFree(p);
     L.ws_allocs.clear();
-    for (double* p : L.FL) cudaFree(p);
-    for (double* p : L.FU) cudaFree(p);
+    for (void* p : L.fac_slabs) cudaFree(p);
+    L.fac_slabs.clear();
+    L.FL.clear();
+    L.FU.clear();
     for (auto& sp : L.spk) {
         for (double* p : sp.GF) if (p) cudaFree(p);
         for (double* p : sp.GB) if (p) cudaFree(p);
@@ -852,12 +855,17 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
         return std::chrono::duration<double, std::milli>(b - a).count();
     };
     const auto t0 = now();
-    for (int f = 0; f < nf; ++f) {
-        double *fl = nullptr, *fu = nullptr;
-        CU(cudaMalloc(&fl, fbytes));
-        CU(cudaMalloc(&fu, fbytes));
-        L.FL.push_back(fl);
-        L.FU.push_back(fu);
+    // all factors of the call in one allocation (fbytes is a multiple of
+    // 16 B: whole operand blocks), one scratch slab below: a cudaMalloc per
+    // factor cost 0.1-0.8 s of host time per call on a busy box (measured)
+    {
+        char* slab = nullptr;
+        CU(cudaMalloc(&slab, 2 * (size_t)nf * fbytes));
+        L.fac_slabs.push_back(slab);
+        for (int f = 0; f < nf; ++f) {
+            L.FL.push_back(reinterpret_cast<double*>(slab + (2 * (size_t)f) * fbytes));
+            L.FU.push_back(reinterpret_cast<double*>(slab + (2 * (size_t)f + 1) * fbytes));
+        }
     }
     const int total = (int)L.FL.size();
     for (auto& sp : L.spk) {
@@ -889,18 +897,20 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     std::vector<double*> lbs(nf, nullptr);
     double** d_lb = nullptr;
     double* d_c = nullptr;
+    char* lslab = nullptr;
     struct Scratch {
-        std::vector<double*>& lbs;
+        char*& lslab;
         double**& d_lb;
         double*& d_c;
         ~Scratch() {
-            for (double* p : lbs) if (p) cudaFree(p);
+            if (lslab) cudaFree(lslab);
             if (d_lb) cudaFree(d_lb);
             if (d_c) cudaFree(d_c);
         }
-    } scratch{lbs, d_lb, d_c};
-    const size_t lbytes = (size_t)L.n * (L.bw + 1) * sizeof(double);
-    for (int f = 0; f < nf; ++f) CU(cudaMalloc(&lbs[f], lbytes));
+    } scratch{lslab, d_lb, d_c};
+    const size_t lbytes = ((size_t)L.n * (L.bw + 1) * sizeof(double) + 255) & ~(size_t)255;
+    CU(cudaMalloc(&lslab, (size_t)nf * lbytes));
+    for (int f = 0; f < nf; ++f) lbs[f] = reinterpret_cast<double*>(lslab + (size_t)f * lbytes);
     // plain allocations, freed after the status sync below: the stream-ordered
     // pool grew (and re-mapped) ~0.5 GB of scratch per call, which cost up to
     // 0.4 s on a box with another problem resident (measured)
@@ -1262,7 +1272,22 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         for (int u = 1; u <= L.U; ++u) ra.off[u] = L.off[u];
         static const int rhs_sm = env_flag("PG_RHS_SM", 0);       // dev A/B
         const int ldh = (256 + 2 * L.omax + 255) / 256;        // halo loads per thread
-        if (rhs_sm && ldh <= 4) {
+        if (rhs_sm == 2 && ldh <= 4) {
+            dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
+            const size_t smr = (size_t)8 * (256 + 2 * L.omax) * sizeof(double);
+            static bool cp_attr = false;
+            if (!cp_attr) {
+                CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+                CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+                CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+                cp_attr = true;
+            }
+            switch (ldh) {
+                case 1: case 2: k_band_rhs_cp<8, 2><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
+                case 3: k_band_rhs_cp<8, 3><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
+                default: k_band_rhs_cp<8, 4><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
+            }
+        } else if (rhs_sm == 1 && ldh <= 4) {
             dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
             const size_t smr = (size_t)2 * (256 + 2 * L.omax) * sizeof(double);
             switch (ldh) {
