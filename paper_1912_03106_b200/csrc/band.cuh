@@ -1261,105 +1261,6 @@ k_band_rhs_dia(RhsDia a, const double* __restrict__ u_prev, const double* __rest
     }
 }
 
-// Same rhs, staged: CTA = (row tile of BD_RHS_R rows, BD_RHS_CC columns).
-// Each column's halo u[perm[j]][r0 - omax, r1 + omax) is read once with
-// coalesced loads into a 2-slot smem ring (the next column's loads are in
-// registers while the current one is computed), so HBM sees each u row once
-// (+ halo re-reads from L2) and the 2U + 1 stencil reads hit shared memory
-// instead of L1.  The M coefficients and source shapes of the thread's
-// BD_RHS_RT rows stay in registers across the columns.  Arithmetic (and its
-// order) is k_band_rhs_dia's, so Y is bit-identical.
-// RT rows per thread (tile = 256 RT rows), LD halo doubles per thread in flight
-template <int RT, int LD>
-__global__ void __launch_bounds__(256)
-k_band_rhs_sm(RhsDia a, const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
-              const double* __restrict__ src, const int* __restrict__ perm,
-              double* __restrict__ Y) {
-    extern __shared__ double su[];           // [2][span]
-    __shared__ int sp[BD_RHS_CC];
-    __shared__ double sc[BD_RHS_CC], ss[BD_RHS_CC][BD_RHS_SRC];
-    const int gc0 = blockIdx.y * BD_RHS_CC;
-    const int ncol = min(BD_RHS_CC, a.B - gc0);
-    for (int t = threadIdx.x; t < BD_RHS_CC * BD_RHS_SRC; t += blockDim.x) {
-        const int j = t / BD_RHS_SRC, q = t % BD_RHS_SRC;
-        const int b = j < ncol ? perm[gc0 + j] : 0;
-        if (q == 0) {
-            sp[j] = b;
-            sc[j] = j < ncol ? inv_dt[b] : 0.0;
-        }
-        ss[j][q] = (j < ncol && q < a.n_src) ? src[(size_t)b * a.n_src + q] : 0.0;
-    }
-    const int omax = a.off[a.U];
-    const int r0 = blockIdx.x * (256 * RT);
-    const int lo = r0 - omax;
-    const int span = (256 * RT) + 2 * omax;
-    // per-row stencil coefficients (k_band_rhs_dia's, absent terms -> 0 at offset 0)
-    double m0[RT], mup[RT][4], mlo[RT][4], sh[RT][BD_RHS_SRC];
-    int oup[RT][4], olo[RT][4];
-    bool has_src[RT];
-#pragma unroll
-    for (int k = 0; k < RT; ++k) {
-        const int i = min(r0 + threadIdx.x + 256 * k, a.n - 1);
-        m0[k] = a.mk[i].x;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int o = a.off[u + 1];
-            const bool on = u < a.U;
-            const bool hu = on && i + o < a.n, hl = on && i - o >= 0;
-            mup[k][u] = hu ? a.mk[(size_t)(u + 1) * a.n + i].x : 0.0;
-            mlo[k][u] = hl ? a.mk[(size_t)(u + 1) * a.n + i - o].x : 0.0;
-            oup[k][u] = hu ? o : 0;
-            olo[k][u] = hl ? -o : 0;
-        }
-        has_src[k] = false;
-#pragma unroll
-        for (int q = 0; q < BD_RHS_SRC; ++q) {
-            sh[k][q] = q < a.n_src ? a.shapes[(size_t)q * a.n + i] : 0.0;
-            has_src[k] |= sh[k][q] != 0.0;
-        }
-    }
-    __syncthreads();
-    double nx[LD];
-    auto fetch = [&](int j) {
-        const double* ub = u_prev + (size_t)sp[j] * a.n;
-#pragma unroll
-        for (int t = 0; t < LD; ++t) {
-            const int jj = threadIdx.x + 256 * t;
-            const int g = lo + jj;
-            nx[t] = (jj < span && g >= 0 && g < a.n) ? __ldg(ub + g) : 0.0;
-        }
-    };
-    if (ncol > 0) fetch(0);
-    for (int j = 0; j < ncol; ++j) {
-        double* s = su + (size_t)(j & 1) * span;
-#pragma unroll
-        for (int t = 0; t < LD; ++t) {
-            const int jj = threadIdx.x + 256 * t;
-            if (jj < span) s[jj] = nx[t];
-        }
-        __syncthreads();
-        if (j + 1 < ncol) fetch(j + 1);
-#pragma unroll
-        for (int k = 0; k < RT; ++k) {
-            const int i = r0 + threadIdx.x + 256 * k;
-            if (i >= a.ldy) continue;
-            double* yo = Y + (size_t)(gc0 + j) * a.ldy + i;
-            if (i >= a.n) { *yo = 0.0; continue; }
-            const double* ub = s + (i - lo);
-            double v = m0[k] * ub[0];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                v = fma(mup[k][u], ub[oup[k][u]], fma(mlo[k][u], ub[olo[k][u]], v));
-            double f = 0.0;
-            if (has_src[k]) {
-#pragma unroll
-                for (int q = 0; q < BD_RHS_SRC; ++q) f = fma(ss[j][q], sh[k][q], f);
-            }
-            *yo = fma(sc[j], v, f);
-        }
-    }
-}
-
 // Same rhs, S-stage cp.async ring: the halos of the next S - 1 columns are in
 // flight (LDGSTS, zero-filled outside [0, n)) while column j is computed from
 // shared memory -- bytes in flight per CTA no longer depend on registers.

@@ -1270,30 +1270,26 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     if (L.dia && !copy_src && L.n_src <= BD_RHS_SRC && L.U <= 4 && env_flag("PG_RHS_DIA", 1)) {
         RhsDia ra{L.n, L.np, B, L.U, L.n_src, {0, 0, 0, 0, 0}, L.mk, L.shapes};
         for (int u = 1; u <= L.U; ++u) ra.off[u] = L.off[u];
-        static const int rhs_sm = env_flag("PG_RHS_SM", 0);       // dev A/B
+        static const int rhs_sm = env_flag("PG_RHS_SM", 2);  // 0 = k_band_rhs_dia (A/B)
         const int ldh = (256 + 2 * L.omax + 255) / 256;        // halo loads per thread
-        if (rhs_sm == 2 && ldh <= 4) {
+        if (rhs_sm == 2 && ldh <= 5) {
+            // cp.async ring: 8 column slots (6 for the 511^2 grid's 1,278-row halo)
             dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
-            const size_t smr = (size_t)8 * (256 + 2 * L.omax) * sizeof(double);
+            const int S = ldh <= 4 ? 8 : 6;
+            const size_t smr = (size_t)S * (256 + 2 * L.omax) * sizeof(double);
             static bool cp_attr = false;
             if (!cp_attr) {
                 CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
                 CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
                 CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+                CU(cudaFuncSetAttribute(k_band_rhs_cp<6, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
                 cp_attr = true;
             }
             switch (ldh) {
                 case 1: case 2: k_band_rhs_cp<8, 2><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
                 case 3: k_band_rhs_cp<8, 3><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
-                default: k_band_rhs_cp<8, 4><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
-            }
-        } else if (rhs_sm == 1 && ldh <= 4) {
-            dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
-            const size_t smr = (size_t)2 * (256 + 2 * L.omax) * sizeof(double);
-            switch (ldh) {
-                case 1: case 2: k_band_rhs_sm<1, 2><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
-                case 3: k_band_rhs_sm<1, 3><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
-                default: k_band_rhs_sm<1, 4><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
+                case 4: k_band_rhs_cp<8, 4><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
+                default: k_band_rhs_cp<6, 5><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
             }
         } else {
             dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
