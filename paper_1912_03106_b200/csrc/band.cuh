@@ -1278,7 +1278,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <int S, int LD>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k_band_rhs_cp(RhsDia a, const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
               const double* __restrict__ src, const int* __restrict__ perm,
               double* __restrict__ Y) {
@@ -1322,44 +1322,68 @@ k_band_rhs_cp(RhsDia a, const double* __restrict__ u_prev, const double* __restr
         has_src |= sh[q] != 0.0;
     }
     __syncthreads();
-    auto issue = [&](int j) {
+    // slot stride SL is a compile-time constant and the column loop is
+    // unrolled by S, so every smem address is (per-thread register + immediate)
+    constexpr int SL = 256 * LD;
+    bool okv[LD];
+    int goff[LD];
+#pragma unroll
+    for (int t = 0; t < LD; ++t) {
+        const int jj = threadIdx.x + 256 * t;
+        const int g = lo + jj;
+        okv[t] = jj < span && g >= 0 && g < a.n;
+        goff[t] = okv[t] ? g : 0;
+    }
+    const uint32_t s_dst = smem_u32(su) + 8u * threadIdx.x;
+    auto issue = [&](int j, int slot) {
         const double* ub = u_prev + (size_t)sp[j] * a.n;
-        double* s = su + (size_t)(j % S) * span;
 #pragma unroll
         for (int t = 0; t < LD; ++t) {
-            const int jj = threadIdx.x + 256 * t;
-            if (jj < span) {
-                const int g = lo + jj;
-                const bool ok = g >= 0 && g < a.n;
-                cp_async8(s + jj, ok ? ub + g : ub, ok ? 8 : 0);
-            }
+            if (threadIdx.x + 256 * t < span)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
+                             ::"r"(s_dst + 8u * (slot * SL + 256 * t)), "l"(ub + goff[t]),
+                             "r"(okv[t] ? 8 : 0)
+                             : "memory");
         }
     };
 #pragma unroll
     for (int j = 0; j < S - 1; ++j) {
-        if (j < ncol) issue(j);
+        if (j < ncol) issue(j, j);
         cp_async_commit();
     }
-    for (int j = 0; j < ncol; ++j) {
-        cp_async_wait<S - 2>();
-        __syncthreads();                 // column j landed; slot (j - 1) % S is free
-        if (j + S - 1 < ncol) issue(j + S - 1);
-        cp_async_commit();
-        if (i < a.ldy) {
-            double* yo = Y + (size_t)(gc0 + j) * a.ldy + i;
-            if (i >= a.n) {
-                *yo = 0.0;
-            } else {
-                const double* ub = su + (size_t)(j % S) * span + (i - lo);
-                double v = m0 * ub[0];
+    const bool row_ok = i < a.n;
+    const int own = i - lo;
+    const double* sb = su + (row_ok ? own : 0);
+    const double* pu[4];
+    const double* pl[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) v = fma(mup[u], ub[oup[u]], fma(mlo[u], ub[olo[u]], v));
-                double f = 0.0;
-                if (has_src) {
+    for (int u = 0; u < 4; ++u) { pu[u] = sb + oup[u]; pl[u] = sb + olo[u]; }
+    double* yrow = Y + (size_t)gc0 * a.ldy + i;
+    for (int j0 = 0; j0 < ncol; j0 += S) {
 #pragma unroll
-                    for (int q = 0; q < BD_RHS_SRC; ++q) f = fma(ss[j][q], sh[q], f);
+        for (int s = 0; s < S; ++s) {
+            const int j = j0 + s;
+            if (j >= ncol) break;
+            cp_async_wait<S - 2>();
+            __syncthreads();             // column j landed; slot (s - 1) % S is free
+            if (j + S - 1 < ncol) issue(j + S - 1, (s + S - 1) % S);
+            cp_async_commit();
+            if (i < a.ldy) {
+                double* yo = yrow + (size_t)j * a.ldy;
+                if (!row_ok) {
+                    *yo = 0.0;
+                } else {
+                    double v = m0 * sb[s * SL];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        v = fma(mup[u], pu[u][s * SL], fma(mlo[u], pl[u][s * SL], v));
+                    double f = 0.0;
+                    if (has_src) {
+#pragma unroll
+                        for (int q = 0; q < BD_RHS_SRC; ++q) f = fma(ss[j][q], sh[q], f);
+                    }
+                    *yo = fma(sc[j], v, f);
                 }
-                *yo = fma(sc[j], v, f);
             }
         }
     }

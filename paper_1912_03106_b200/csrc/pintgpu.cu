@@ -1276,7 +1276,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             // cp.async ring: 8 column slots (6 for the 511^2 grid's 1,278-row halo)
             dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
             const int S = ldh <= 4 ? 8 : 6;
-            const size_t smr = (size_t)S * (256 + 2 * L.omax) * sizeof(double);
+            const size_t smr = (size_t)S * 256 * std::max(ldh, 2) * sizeof(double);  // slot stride 256 LD
             static bool cp_attr = false;
             if (!cp_attr) {
                 CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
