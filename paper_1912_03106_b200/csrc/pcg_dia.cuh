@@ -37,6 +37,13 @@ struct DiaLevel {
     int off[PG_DIA_MAX + 1];    // off[0] = 0
     int omax;
     const double2* __restrict__ mk;    // [(U+1)][n] (m, k)
+    // uniform-1/dt fast path (k_dia_cb0, every call): for columns whose 1/dt
+    // equals *cb0 the kernels read a0 = fma(cb0, M, K) per entry and
+    // dinv0 = 1/(cb0 M_ii + K_ii) -- the same expressions the generic path
+    // evaluates per column, so results are bit-identical
+    const double* __restrict__ a0;     // [(U+1)][n]
+    const double* __restrict__ dinv0;  // [ld], 0 on padding rows
+    const double* __restrict__ cb0;    // [1]
     int n_src;
     const double* __restrict__ shapes;
     int R, n_tiles;
@@ -89,6 +96,22 @@ __device__ __forceinline__ void tile_span(const DiaLevel& L, int tile, int& r0, 
     r1 = min(L.n, r0 + L.R);
     lo = max(0, r0 - L.omax) & ~1;            // even -> 16-byte aligned pairs
     hi = min(L.ld, (r1 + L.omax + 1) & ~1);   // even, within the padded row
+}
+
+// a0 / dinv0 / cb0 for cb0 = inv_dt[0]
+__global__ void k_dia_cb0(DiaLevel L, double* __restrict__ a0, double* __restrict__ dinv0,
+                          double* __restrict__ cb0, const double* __restrict__ inv_dt) {
+    const double cb = inv_dt[0];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *cb0 = cb;
+    if (i >= L.ld) return;
+    if (i >= L.n) { dinv0[i] = 0.0; return; }
+    const double2 d = L.mk[i];
+    dinv0[i] = dinv_of(cb, d.x, d.y);
+    for (int u = 0; u <= L.U; ++u) {
+        const double2 e = L.mk[(size_t)u * L.n + i];
+        a0[(size_t)u * L.n + i] = fma(cb, e.x, e.y);
+    }
 }
 
 // --- setup: x0 = guess or u_prev, r0 = b - A x0, |b|^2, rho0 ----------------------
@@ -305,6 +328,12 @@ k_sdir(DiaLevel L, DiaWork V, PcgWork W, double* __restrict__ qv, int cur,
         cbv[c] = inv_dt[bv[c]];
         betav[c] = W.beta[bv[c]];
     }
+    bool same = true;
+    {
+        const double c0 = *L.cb0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) same &= (c >= nc) || cbv[c] == c0;
+    }
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         mbar_fence_init();
@@ -324,8 +353,13 @@ k_sdir(DiaLevel L, DiaWork V, PcgWork W, double* __restrict__ qv, int cur,
     // p_new over the halo, in place (column-major loop so D^-1 loads are shared)
     for (int jj = 2 * threadIdx.x; jj < span; jj += 2 * PG_DIA_NT) {
         const int j = lo + jj;
-        const double2 d0 = j < L.n ? __ldg(L.mk + j) : make_double2(1.0, 1.0);
-        const double2 d1 = j + 1 < L.n ? __ldg(L.mk + j + 1) : make_double2(1.0, 1.0);
+        double2 d0, d1, dv;
+        if (same) {
+            dv = __ldg(reinterpret_cast<const double2*>(L.dinv0 + j));
+        } else {
+            d0 = j < L.n ? __ldg(L.mk + j) : make_double2(1.0, 1.0);
+            d1 = j + 1 < L.n ? __ldg(L.mk + j + 1) : make_double2(1.0, 1.0);
+        }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if (c >= nc) break;
@@ -333,8 +367,13 @@ k_sdir(DiaLevel L, DiaWork V, PcgWork W, double* __restrict__ qv, int cur,
             double* sp = sr + SPAN;
             const double2 rv = *reinterpret_cast<const double2*>(sr + jj);
             double2 o;
-            o.x = rv.x * dinv_of(cbv[c], d0.x, d0.y);
-            o.y = rv.y * dinv_of(cbv[c], d1.x, d1.y);
+            if (same) {
+                o.x = rv.x * dv.x;
+                o.y = rv.y * dv.y;
+            } else {
+                o.x = rv.x * dinv_of(cbv[c], d0.x, d0.y);
+                o.y = rv.y * dinv_of(cbv[c], d1.x, d1.y);
+            }
             if (!firstv[c]) {
                 const double2 pv = *reinterpret_cast<const double2*>(sp + jj);
                 o.x = fma(betav[c], pv.x, o.x);
@@ -347,6 +386,36 @@ k_sdir(DiaLevel L, DiaWork V, PcgWork W, double* __restrict__ qv, int cur,
     double pq[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) pq[c] = 0.0;
+    if (same) {
+        for (int i = r0 + threadIdx.x; i < r1; i += PG_DIA_NT) {
+            // a0 entries: the row's diagonal, U upper and U mirrored lower
+            const double ad = __ldg(L.a0 + i);
+            double au[UU], al[UU];
+#pragma unroll
+            for (int u = 1; u <= UU; ++u) {
+                const int o = L.off[u];
+                au[u - 1] = __ldg(L.a0 + (size_t)u * L.n + i);
+                al[u - 1] = (i - o >= 0) ? __ldg(L.a0 + (size_t)u * L.n + i - o) : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if (c >= nc) break;
+                const double* spw = smem + (size_t)c * 2 * SPAN + SPAN - lo;
+                double q = ad * spw[i];             // dia_row with fma(cb, m, k) precomputed
+#pragma unroll
+                for (int u = 1; u <= UU; ++u) {
+                    const int o = L.off[u];
+                    if (i + o < L.n) q = fma(au[u - 1], spw[i + o], q);
+                    if (i - o >= 0) q = fma(al[u - 1], spw[i - o], q);
+                }
+                const double pi = spw[i];
+                pq[c] = fma(pi, q, pq[c]);
+                const size_t k = (size_t)bv[c] * L.ld + i;
+                p_new[k] = pi;
+                qv[k] = q;
+            }
+        }
+    } else
     for (int i = r0 + threadIdx.x; i < r1; i += PG_DIA_NT) {
         double2 dg, up[UU], lw[UU];
         dia_load_row<UU>(L, i, dg, up, lw);
@@ -411,6 +480,7 @@ k_supd(DiaLevel L, DiaWork V, PcgWork W, const double* __restrict__ qv, int cur,
     if (slot < na) {
         const int b = W.act[cur][slot];
         const double cb = inv_dt[b];
+        const bool same = cb == *L.cb0;
         const double al = W.alpha[b];
         const size_t base = (size_t)b * L.ld;
         const double* __restrict__ p = V.p[cur ^ 1] + base;
@@ -434,8 +504,15 @@ k_supd(DiaLevel L, DiaWork V, PcgWork W, const double* __restrict__ qv, int cur,
         for (int k = 0; k < PG_UPD_V; ++k) {
             const int i = i0 + 2 * (threadIdx.x + k * PG_UPD_NT);
             if (i < L.n) {
-                const double2 d0 = __ldg(L.mk + i);
-                const double2 d1 = (i + 1 < L.n) ? __ldg(L.mk + i + 1) : make_double2(1.0, 1.0);
+                double2 dv;
+                if (same) {
+                    dv = __ldg(reinterpret_cast<const double2*>(L.dinv0 + i));
+                } else {
+                    const double2 d0 = __ldg(L.mk + i);
+                    const double2 d1 = (i + 1 < L.n) ? __ldg(L.mk + i + 1) : make_double2(1.0, 1.0);
+                    dv.x = dinv_of(cb, d0.x, d0.y);
+                    dv.y = dinv_of(cb, d1.x, d1.y);
+                }
                 double2 xo, ro;
                 xo.x = fma(al, pv[k].x, xv[k].x);
                 xo.y = fma(al, pv[k].y, xv[k].y);
@@ -443,10 +520,10 @@ k_supd(DiaLevel L, DiaWork V, PcgWork W, const double* __restrict__ qv, int cur,
                 ro.y = fma(-al, qq[k].y, rv[k].y);   // padding rows: q = r = 0
                 *reinterpret_cast<double2*>(x + i) = xo;
                 *reinterpret_cast<double2*>(r + i) = ro;
-                acc[0] = fma(ro.x * ro.x, dinv_of(cb, d0.x, d0.y), acc[0]);
+                acc[0] = fma(ro.x * ro.x, dv.x, acc[0]);
                 acc[1] = fma(ro.x, ro.x, acc[1]);
                 if (i + 1 < L.n) {
-                    acc[0] = fma(ro.y * ro.y, dinv_of(cb, d1.x, d1.y), acc[0]);
+                    acc[0] = fma(ro.y * ro.y, dv.y, acc[0]);
                     acc[1] = fma(ro.y, ro.y, acc[1]);
                 }
             }

@@ -43,6 +43,9 @@ struct Level {
     int U = 0, omax = 0, ld = 0, Cd = 1;
     int off[PG_DIA_MAX + 1] = {0};
     double2* mk = nullptr;
+    double* a0 = nullptr;          // uniform-1/dt fast path of the DIA PCG
+    double* dinv0 = nullptr;
+    double* cb0 = nullptr;
     DiaWork V{};
     double* qv = nullptr;          // q = A p of the DIA path [B][ld]
     // banded-Cholesky path (per distinct dt factors)
@@ -229,7 +232,7 @@ extern "C" int pg_create(pg_ctx** out, int device) {
 static void free_level(Level& L) {
     void* ptrs[] = {L.row_ptr, L.col_idx, L.m_val, L.k_val, L.dM, L.dK, L.shapes,
                     L.weights, L.tile_lo, L.tile_hi, L.elem_dof, L.elem_geo,
-                    L.ne_ptr, L.ne, L.mk, L.d_FL, L.d_FU, L.Y, L.d_perm,
+                    L.ne_ptr, L.ne, L.mk, L.a0, L.dinv0, L.cb0, L.d_FL, L.d_FU, L.Y, L.d_perm,
                     L.d_chunks, L.d_status, L.k_pre, L.spk_T, L.d_spk_chunks};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -433,6 +436,9 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
                 if (L.dia) {
                     int rc0 = dev_upload(ctx, &L.mk, mk.data(), mk.size());
                     if (rc0) return -1;
+                    CU(cudaMalloc(&L.a0, (size_t)(U + 1) * d->n * sizeof(double)));
+                    CU(cudaMalloc(&L.dinv0, (size_t)L.ld * sizeof(double)));
+                    CU(cudaMalloc(&L.cb0, sizeof(double)));
                 }
             }
         }
@@ -616,6 +622,9 @@ static DiaLevel dia_view(const Level& L) {
     for (int u = 0; u <= PG_DIA_MAX; ++u) v.off[u] = L.off[u];
     v.omax = L.omax;
     v.mk = L.mk;
+    v.a0 = L.a0;
+    v.dinv0 = L.dinv0;
+    v.cb0 = L.cb0;
     v.n_src = L.n_src;
     v.shapes = L.shapes;
     v.R = L.R;
@@ -733,6 +742,8 @@ static int pcg_dia(pg_ctx* ctx, Level& L, int B, const double* u_prev, const dou
         }
         LAUNCHED();
     }
+    k_dia_cb0<<<(L.ld + 255) / 256, 256, 0, st>>>(dia_view(L), L.a0, L.dinv0, L.cb0, inv_dt);
+    LAUNCHED();
     int rc, na = B, cur = 0, it = 0;
     const int K = ctx->opts.check_every;
     if ((rc = poll_nact(ctx, L.W, 0, st, &na))) return rc;

@@ -95,6 +95,37 @@ def test_cholesky_many_dt_and_rhs_add(cuda):
     assert err.max() < 1e-12, err.max()
 
 
+@pytest.mark.parametrize("first_shared", [True, False])
+def test_streamed_pcg_mixed_dt(cuda, first_shared):
+    """Streamed (DIA) Jacobi-PCG with a batch whose columns partly share
+    column 0's 1/dt (the kernels' precomputed uniform-1/dt operands) and
+    partly do not (per-column cb M + K), in either order, vs the oracle."""
+    fx = load_golden("phi_cfg2_n128")
+    from oracle import fem2d
+    prob = _problem(fx["spec"], inner="pcg")
+    ref = fem2d.make_problem(fx["spec"])
+    n = prob.spatial.size(0)
+    rng = np.random.default_rng(11)
+    B = 21
+    U = rng.standard_normal((B, n)) * 1e-3
+    tn = np.sort(rng.uniform(0.001, 0.02, B))
+    k = np.where(rng.uniform(size=B) < 0.5, 1, 1 + rng.integers(1, 5, B))
+    k[0] = 1
+    if not first_shared:
+        k[0] = 3
+    dts = (0.02 / 2 ** 14) * k          # bitwise-equal 1/dt for equal k
+    tp = tn - dts
+    dev = prob.device
+    out = torch.empty(B, n, dtype=torch.float64, device=dev)
+    prob.phi_batch(0, torch.as_tensor(U, device=dev), torch.as_tensor(1.0 / dts, device=dev),
+                   torch.as_tensor(prob.source_values(tn), device=dev), out)
+    got, st = out.cpu().numpy(), prob.last_stats()
+    assert st["failed"] == 0
+    exp = ref.step_batch(U, tp, tn, 0, False)
+    err = np.linalg.norm(got - exp, axis=1) / np.linalg.norm(exp, axis=1)
+    assert err.max() < TOL["pcg"], err.max()
+
+
 def test_phi_guess_and_rhs_add(cuda):
     fx = load_golden("phi_cfg2_n128")
     prob = _problem(fx["spec"])
