@@ -387,6 +387,7 @@ k_sdir(DiaLevel L, DiaWork V, PcgWork W, double* __restrict__ qv, int cur,
 #pragma unroll
     for (int c = 0; c < C; ++c) pq[c] = 0.0;
     if (same) {
+#pragma unroll 2
         for (int i = r0 + threadIdx.x; i < r1; i += PG_DIA_NT) {
             // a0 entries: the row's diagonal, U upper and U mirrored lower
             const double ad = __ldg(L.a0 + i);
