@@ -42,7 +42,9 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // diagonal-block inverse (row stride BD_PD), then NCHK pieces of CW window
 // columns each (row stride CW + 4): every piece is one contiguous TMA copy.
 #define BD_PD 36
-__host__ __device__ __forceinline__ int bd_cw(int W) { return W < 128 ? W : 128; }
+// window chunk width of the operand layout: 64-column chunks for W = 512
+// (17 KB TMA pieces: a 4-deep ring fits beside k_band_rb's 32-column window)
+__host__ __device__ __forceinline__ int bd_cw(int W) { return W < 128 ? W : (W >= 512 ? 64 : 128); }
 __host__ __device__ __forceinline__ size_t bd_block_doubles(int W) {
     return (size_t)32 * (BD_PD + (W / bd_cw(W)) * (bd_cw(W) + 4));
 }
@@ -975,7 +977,10 @@ k_band_pipe(BandSolveArgs a) {
             const int total = nsteps * NPB;
             for (int P = 0; P < total; ++P) {
                 const int buf = P % BD_NBUF, use = P / BD_NBUF;
-                if (use > 0) mbar_wait(&empty[buf], (use - 1) & 1);
+                if (use > 0) {
+                    mbar_wait(&empty[buf], (use - 1) & 1);
+                    fence_proxy_async_smem();   // consumers' generic reads before the refill
+                }
                 const int s = P / NPB, j = P % NPB;
                 const double* src = F + (size_t)blk_of(s) * blk_doubles +
                                     (j == 0 ? 0 : (size_t)NB * BD_PD + (size_t)(j - 1) * NB * (CW + 4));

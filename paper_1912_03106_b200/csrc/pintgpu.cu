@@ -8,6 +8,7 @@
 #include "mgrit_ops.cuh"
 #include "newton.cuh"
 #include "band.cuh"
+#include "band_rb.cuh"
 #include "newton_nk.cuh"
 
 #include <algorithm>
@@ -813,6 +814,19 @@ static int newton_nk(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
                      const double* inv_dt, const double* inv_dt_host, const double* src,
                      double* u_out, const double* g, const int* g_idx, cudaStream_t st);
 
+// dev A/B switches (environment, read once per process)
+static int env_flag(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e && e[0] ? atoi(e) : dflt;
+}
+
+// register-blocked chain (band_rb.cuh) for the multi-column groups;
+// PG_BAND_RB=0 keeps the round-1 kernels (A/B measurements)
+static int band_rb_on() {
+    static const int v = env_flag("PG_BAND_RB", 1);
+    return v;
+}
+
 // ---------------------------------------------------------------------------
 // banded-Cholesky Phi (problems.py:130-146 on the GPU)
 // columns per solve CTA: 8 (one DMMA n-tile) so a batch of B columns spreads
@@ -821,19 +835,20 @@ static int band_solve_bc(const Level& L, int B, int n_sm) {
     if (B <= n_sm) return 1;          // one column per CTA: FMA chain
     if (const char* e = getenv("PG_BAND_BC")) {          // dev override (A/B measurements)
         const int v = atoi(e);
-        if (v == 8 || (v == 16 && L.bwin <= 256)) return v;
+        if (v == 8 || (v == 16 && (L.bwin <= 256 || band_rb_on())) || (v == 32 && band_rb_on()))
+            return v;
+    }
+    if (band_rb_on()) {
+        // widest group that still gives ~one CTA per SM: operand bytes per
+        // column fall with the width (k_band_rb)
+        if (B >= 26 * n_sm) return 32;
+        if (B >= 13 * n_sm) return 16;
+        return 8;
     }
     if (L.bwin >= 512) return 8;      // 17-slot window ring leaves room for 8
     return B >= 16 * n_sm ? 16 : 8;
 }
 
-// smem of the pipelined chain: BD_NBUF operand pieces + (NSLOT+1)-slot
-// window ring + double-buffered b
-// dev A/B switches (environment, read once per process)
-static int env_flag(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e && e[0] ? atoi(e) : dflt;
-}
 
 // k-split factor of the multi-column chain (k_band_chain_ks); PG_BAND_KS=1
 // selects the single-warp-per-row-tile k_band_chain (A/B measurements)
@@ -953,11 +968,53 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     return PG_OK;
 }
 
+// warp tiling (WM x WN x WK consumer warps) per column-group width; the
+// deepest operand ring that fits the 227 KB shared-memory limit
+template <int BC, int CW, int NCHK, bool FWD, int WM, int WN, int WK>
+static int launch_rb_t(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, cudaStream_t st) {
+    constexpr size_t lim = 232448 - 1024;
+    constexpr int NBUF = rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, 4>() <= lim ? 4
+                       : rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, 3>() <= lim ? 3 : 2;
+    constexpr size_t sm = rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, NBUF>();
+    static_assert(sm <= lim, "k_band_rb shared memory");
+    auto k = k_band_rb<BC, CW, NCHK, FWD, WM, WN, WK, NBUF>;
+    CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k<<<grid, 32 * (WM * WN * WK + 1), sm, st>>>(sa);
+    LAUNCHED();
+    return PG_OK;
+}
+
+template <int BC, int CW, int NCHK, bool FWD>
+static int launch_rb(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, cudaStream_t st) {
+    static const int alt = env_flag("PG_RB_ALT", 0);     // dev: alternative tilings
+    if constexpr (BC == 8) {
+        if (alt == 1) return launch_rb_t<BC, CW, NCHK, FWD, 1, 1, 8>(ctx, sa, grid, st);
+        if (alt == 2) return launch_rb_t<BC, CW, NCHK, FWD, 4, 1, 2>(ctx, sa, grid, st);
+        return launch_rb_t<BC, CW, NCHK, FWD, 2, 1, 4>(ctx, sa, grid, st);
+    } else if constexpr (BC == 16) {
+        if (alt == 1) return launch_rb_t<BC, CW, NCHK, FWD, 2, 2, 2>(ctx, sa, grid, st);
+        return launch_rb_t<BC, CW, NCHK, FWD, 2, 1, 4>(ctx, sa, grid, st);
+    } else {
+        if (alt == 1) return launch_rb_t<BC, CW, NCHK, FWD, 4, 2, 1>(ctx, sa, grid, st);
+        return launch_rb_t<BC, CW, NCHK, FWD, 2, 2, 2>(ctx, sa, grid, st);
+    }
+}
+
 // one triangular direction of the batched chain solve: grid (column groups, chunks)
 template <int BC, int CW, int NCHK, bool FWD>
 static int launch_dir(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, size_t sm,
                       cudaStream_t st) {
-    if constexpr (CW * NCHK > 256) {
+    if constexpr (BC >= 8) {
+        // k_band_rb wins for the 512-wide window (operand-stream bound) and
+        // for wide groups; the 8-column chains of narrower windows stay on
+        // k_band_chain_ks (per-step overhead; PG_BAND_RB=2 forces k_band_rb)
+        const int rb = band_rb_on();
+        if (BC == 32 || (rb && (CW * NCHK > 256 || BC >= 16)) || rb == 2)
+            return launch_rb<BC, CW, NCHK, FWD>(ctx, sa, grid, st);
+    }
+    if constexpr (BC == 32) {
+        return PG_EINVAL;
+    } else if constexpr (CW * NCHK > 256) {
         auto k = k_band_pipe<BC, CW, NCHK, FWD>;
         CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k<<<grid, BD_PCT, sm, st>>>(sa);
@@ -990,8 +1047,8 @@ static int launch_dir_bc(pg_ctx* ctx, int BC, bool fwd, const BandSolveArgs& sa,
                : launch_dir<B_, CW, NCHK, false>(ctx, sa, grid, sm, st);
     if (BC == 1) { PG_DIR(1) }
     if (BC == 8) { PG_DIR(8) }
-    if constexpr (CW * NCHK <= 256)
-        if (BC == 16) { PG_DIR(16) }
+    if (BC == 16 && (CW * NCHK <= 256 || band_rb_on())) { PG_DIR(16) }
+    if (BC == 32 && band_rb_on()) { PG_DIR(32) }
 #undef PG_DIR
     return set_err(ctx, PG_EINVAL, "band batch width %d not supported", BC);
 }
@@ -1003,7 +1060,7 @@ static int band_dir(pg_ctx* ctx, const Level& L, int BC, bool fwd, const BandSol
         case 64: return launch_dir_bc<64, 1>(ctx, BC, fwd, sa, grid, sm, st);
         case 128: return launch_dir_bc<128, 1>(ctx, BC, fwd, sa, grid, sm, st);
         case 256: return launch_dir_bc<128, 2>(ctx, BC, fwd, sa, grid, sm, st);
-        case 512: return launch_dir_bc<128, 4>(ctx, BC, fwd, sa, grid, sm, st);
+        case 512: return launch_dir_bc<64, 8>(ctx, BC, fwd, sa, grid, sm, st);
         default: return set_err(ctx, PG_EINVAL, "band window %d not supported", L.bwin);
     }
 }
@@ -1276,7 +1333,8 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     dim3 gr((L.np + 255) / 256, (B + BD_RHS_CB - 1) / BD_RHS_CB);
     // the scatter (unpartitioned chains) is fused into the k-split backward chain
     const int ksv = band_ks();
-    const bool fuse = BC >= 8 && L.bwin <= 256 && (ksv == 2 || ksv == 4) &&
+    const bool fuse = BC >= 8 && ((band_rb_on() && (L.bwin > 256 || BC >= 16)) ||
+                                  band_rb_on() == 2 || (L.bwin <= 256 && (ksv == 2 || ksv == 4))) &&
                       env_flag("PG_BAND_FUSE", 1);
     if (L.dia && !copy_src && L.n_src <= BD_RHS_SRC && L.U <= 4 && env_flag("PG_RHS_DIA", 1)) {
         RhsDia ra{L.n, L.np, B, L.U, L.n_src, {0, 0, 0, 0, 0}, L.mk, L.shapes};
@@ -1614,5 +1672,19 @@ extern "C" int pg_profile_read(pg_ctx* ctx, pg_kernel_profile* out, int n, int r
         }
         ctx->prof_cols = 0;
     }
+    return PG_OK;
+}
+
+// dev-only (not in pintgpu.h): copy the SPIKE response G of (level,
+// partition, factor, direction) into out ([W][np] doubles, device); returns
+// PG_EINVAL when it has not been computed
+extern "C" int pg_dev_spike_g(pg_ctx* ctx, int level, int pi, int f, int fwd, double* out) {
+    if (!ctx || level < 0 || level >= (int)ctx->levels.size() || pi < 0 || pi > 2) return PG_EINVAL;
+    Level& L = ctx->levels[level];
+    const Level::SpikePart& sp = L.spk[pi];
+    if (f < 0 || f >= (int)sp.GF.size()) return PG_EINVAL;
+    const double* G = fwd ? sp.GF[f] : sp.GB[f];
+    if (!G) return PG_EINVAL;
+    CU(cudaMemcpy(out, G, (size_t)L.bwin * L.np * sizeof(double), cudaMemcpyDeviceToDevice));
     return PG_OK;
 }

@@ -1,5 +1,5 @@
 """Per-(level, batch) time breakdown of the batched Phi calls inside one
-config-2 MGRIT solve (dev tool; CUDA events around every call)."""
+config-2/3/4 MGRIT solve (dev tool; CUDA events around every call)."""
 import collections, json, sys, time
 import torch
 sys.path.insert(0, '.')
@@ -7,8 +7,16 @@ from paper_1912_03106_b200 import (GpuFemProblem, CycleSpec, StoppingCriterion, 
                                    build_uniform_grid, MgritSolver, configs, build)
 build.build()
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-spec = (configs.config2(grids=2, strategy="delayed") if name == "cfg2"
-        else configs.config3(grids=2, strategy="delayed"))
+if name == "cfg2":
+    spec = configs.config2(grids=2, strategy="delayed")
+elif name == "cfg3":
+    spec = configs.config3(grids=2, strategy="delayed")
+elif name == "cfg4":
+    spec = configs.config4(grids=2, strategy="delayed")
+elif name == "cfg4s":
+    spec = configs.config2(N=128, n_steps=2 ** 14, levels=4, grids=2, strategy="delayed")
+else:
+    raise SystemExit(name)
 if "merge" in sys.argv[2:]:
     spec["inner"]["dt_merge_rtol"] = 1e-12
 prob = GpuFemProblem(spec)
