@@ -19,7 +19,7 @@ See DESIGN.md for the data layout, kernels and rooflines.
 """
 
 from . import configs
-from .errors import NewtonConvergenceError, PintGpuError, TransportError
+from .errors import InnerSolveError, NewtonConvergenceError, PintGpuError, TransportError
 from .excitation import Excitation
 from .mgrit import (CycleSpec, MgritSolver, SolverRun, StoppingCriterion,
                     StorageReport, mgrit_solve, qoi_change, sequential_solve,
@@ -35,7 +35,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BlockState", "CFSplitting", "CycleSpec", "Decomposition", "DistTransport",
-    "Excitation", "GpuFemProblem", "GpuSurrogateProblem", "make_problem", "MgritSolver", "NewtonConvergenceError",
+    "Excitation", "GpuFemProblem", "GpuSurrogateProblem", "InnerSolveError", "make_problem",
+    "MgritSolver", "NewtonConvergenceError",
     "NullTransport", "PintGpuError", "SolverRun", "SpaceTimeVector",
     "SpatialHierarchy2D", "StepDiagnostics", "StoppingCriterion", "StorageReport",
     "TimeGrid", "TimeHierarchy", "TransportError", "assign_spatial_levels",

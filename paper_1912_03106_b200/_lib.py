@@ -8,7 +8,7 @@ library is missing, and pg_create fails without a CUDA device.
 import ctypes
 import os
 
-from .errors import NewtonConvergenceError, PintGpuError
+from .errors import InnerSolveError, NewtonConvergenceError, PintGpuError
 
 # PINTGPU_LIB: dev override for A/B builds of the library
 LIB_PATH = os.environ.get("PINTGPU_LIB") or os.path.join(
@@ -117,6 +117,8 @@ def check(ctx, rc, what):
         raise ValueError(f"{what}: {msg}")
     if rc == PG_ENEWTON:
         raise NewtonConvergenceError(f"{what}: {msg}")
+    if rc == PG_ENOCONV:
+        raise InnerSolveError(f"{what}: {msg}")
     raise PintGpuError(f"{what} failed with code {rc}: {msg}")
 
 

@@ -206,10 +206,12 @@ k_nk_cg_b(int n, const int* __restrict__ act, const double* __restrict__ R,
     __shared__ double red[2 * (NK_NT / 32) + 2];
     const int b = act[blockIdx.x];
     const size_t off = (size_t)b * n;
+    // read rho before the reduction's barriers: thread 0 overwrites it below
+    const double rho_old = rho[b];
     double acc = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) acc = fma(R[off + i], Z[off + i], acc);
     const double rz = nk_sum(acc, red);
-    const double beta = first ? 0.0 : rz / rho[b];
+    const double beta = first ? 0.0 : rz / rho_old;
     for (int i = threadIdx.x; i < n; i += blockDim.x)
         P[off + i] = first ? Z[off + i] : fma(beta, P[off + i], Z[off + i]);
     if (threadIdx.x == 0) rho[b] = rz;

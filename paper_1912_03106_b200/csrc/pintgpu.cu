@@ -12,6 +12,7 @@
 #include "newton_nk.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdarg>
 #include <cstdlib>
@@ -164,6 +165,20 @@ static int set_err(pg_ctx* ctx, int code, const char* fmt, ...) {
         if (e_ != cudaSuccess)                                                 \
             return set_err(ctx, PG_ECUDA, "%s:%d launch: %s", __FILE__,        \
                            __LINE__, cudaGetErrorString(e_));                  \
+    } while (0)
+
+// cudaFuncSetAttribute is per device: set a kernel's dynamic-smem limit
+// once per (call site, device), thread-safely (a second pg_ctx on another
+// device in the same process gets its own attribute)
+#define SMEM_ATTR_ONCE(fn, bytes)                                                          \
+    do {                                                                                   \
+        static std::atomic<uint64_t> done_{0};                                             \
+        const uint64_t bit_ = 1ull << (ctx->device & 63);                                  \
+        if (!(done_.load(std::memory_order_acquire) & bit_)) {                             \
+            CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                    (int)(bytes)));                                        \
+            done_.fetch_or(bit_, std::memory_order_release);                               \
+        }                                                                                  \
     } while (0)
 
 template <typename T>
@@ -578,14 +593,8 @@ static int launch_iter(pg_ctx* ctx, Level& L, int ny, int cur, const double* inv
                        double* x, cudaStream_t st) {
     dim3 grid(L.n_tiles, ny);
     size_t sm = stream_smem(L, C, false);
-    static bool attr_done = false;   // per template instance
-    if (!attr_done) {
-        CU(cudaFuncSetAttribute(k_pcg_dir<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                96 * 1024 + 1024));
-        CU(cudaFuncSetAttribute(k_pcg_upd<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                96 * 1024 + 1024));
-        attr_done = true;
-    }
+    SMEM_ATTR_ONCE(k_pcg_dir<C>, 96 * 1024 + 1024);
+    SMEM_ATTR_ONCE(k_pcg_upd<C>, 96 * 1024 + 1024);
     k_pcg_dir<C><<<grid, PG_NT, sm, st>>>(pcg_view(L), L.W, cur, inv_dt);
     LAUNCHED();
     k_pcg_upd<C><<<grid, PG_NT, sm, st>>>(pcg_view(L), L.W, cur, inv_dt, x,
@@ -676,12 +685,7 @@ static int launch_dia_iter_c(pg_ctx* ctx, Level& L, int na, int cur, const doubl
                              cudaStream_t st) {
     const int SPAN = (L.R + 2 * L.omax + 4) & ~1;
     const size_t sm = (size_t)C * 2 * SPAN * sizeof(double);
-    static bool attr_done = false;
-    if (!attr_done) {
-        CU(cudaFuncSetAttribute(k_sdir<C, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                200 * 1024));
-        attr_done = true;
-    }
+    SMEM_ATTR_ONCE((k_sdir<C, UU>), 200 * 1024);
     int rc;
     if ((rc = prof_mark(ctx, 0, st))) return rc;
     dim3 gd(L.n_tiles, (na + C - 1) / C);
@@ -1346,14 +1350,10 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
             const int S = ldh <= 4 ? 8 : 6;
             const size_t smr = (size_t)S * 256 * std::max(ldh, 2) * sizeof(double);  // slot stride 256 LD
-            static bool cp_attr = false;
-            if (!cp_attr) {
-                CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-                CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-                CU(cudaFuncSetAttribute(k_band_rhs_cp<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-                CU(cudaFuncSetAttribute(k_band_rhs_cp<6, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-                cp_attr = true;
-            }
+            SMEM_ATTR_ONCE((k_band_rhs_cp<8, 2>), 96 * 1024);
+            SMEM_ATTR_ONCE((k_band_rhs_cp<8, 3>), 96 * 1024);
+            SMEM_ATTR_ONCE((k_band_rhs_cp<8, 4>), 96 * 1024);
+            SMEM_ATTR_ONCE((k_band_rhs_cp<6, 5>), 96 * 1024);
             switch (ldh) {
                 case 1: case 2: k_band_rhs_cp<8, 2><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
                 case 3: k_band_rhs_cp<8, 3><<<grd, 256, smr, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y); break;
@@ -1442,6 +1442,19 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     return PG_OK;
 }
 
+// Jacobi-PCG columns that stopped at max_iters above rtol make the call fail
+// (PG_ENOCONV): the engine must not accept an unconverged Phi.  The direct
+// solve of the reference (problems.py:130-146) cannot fail this way.
+static int pcg_check_converged(pg_ctx* ctx, int B, cudaStream_t st) {
+    CU(cudaMemcpyAsync(ctx->h_poll + 4, ctx->d_ictr + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const int failed = ctx->h_poll[4];
+    if (failed > 0)
+        return set_err(ctx, PG_ENOCONV, "%d of %d columns hit max_iters (%d) above rtol %.3g",
+                       failed, B, ctx->opts.max_iters, ctx->opts.rtol);
+    return PG_OK;
+}
+
 extern "C" int pg_prefactor(pg_ctx* ctx, int level, int n, const double* inv_dt_host,
                             void* stream) {
     if (!ctx) return PG_EINVAL;
@@ -1508,11 +1521,15 @@ extern "C" int pg_phi_batch_h(pg_ctx* ctx, int level, int B, const double* u_pre
     } else if (ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok) {
         return band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
     } else if (L.resident) {
-        return launch_resident(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st);
+        if ((rc = launch_resident(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st)))
+            return rc;
+        return pcg_check_converged(ctx, B, st);
     } else if (L.dia) {
-        return pcg_dia(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st);
+        if ((rc = pcg_dia(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st))) return rc;
+        return pcg_check_converged(ctx, B, st);
     } else {
         if ((rc = pcg_streamed(ctx, L, B, u_prev, guess, inv_dt, src, u_out, st))) return rc;
+        if ((rc = pcg_check_converged(ctx, B, st))) return rc;
     }
     if (g) {
         dim3 grid(std::max(1, std::min(64, (L.n + 255) / 256)), B);

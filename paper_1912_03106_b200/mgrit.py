@@ -259,18 +259,31 @@ class MgritSolver:
     def _phi_off(self, lvl, U, j, out, add_rhs=True):
         """Offset-j step of every owned interval: out = Phi(U) (+ rhs)."""
         use_g = add_rhs and lvl.use_rhs
-        self.problem.phi_batch(lvl.s, U, lvl.inv_dt_off[j], lvl.src_off[self._smooth][j], out,
-                               g=lvl.rhs if use_g else None,
-                               g_idx=lvl.gidx_off[j] if use_g else None,
-                               **self._host_dt(lvl.inv_dt_off_h[j]))
+        try:
+            self.problem.phi_batch(lvl.s, U, lvl.inv_dt_off[j], lvl.src_off[self._smooth][j],
+                                   out, g=lvl.rhs if use_g else None,
+                                   g_idx=lvl.gidx_off[j] if use_g else None,
+                                   **self._host_dt(lvl.inv_dt_off_h[j]))
+        except NewtonConvergenceError as e:
+            # t_next of the failing interval's step (problems.py:240-244)
+            col = getattr(e, "column", -1)
+            if 0 <= col < len(lvl.c_idx):
+                e.at_time(lvl.t[lvl.c_idx[col] - lvl.m + j], lvl.s)
+            raise
         self.phi_columns += U.shape[0]
         self.phi_calls += 1
 
     def _phi_pts(self, lvl, U, lo, hi, out, g=None, g_idx=None):
         """Consecutive points lo..hi-1 of lvl's grid, one column each."""
-        self.problem.phi_batch(lvl.s, U, lvl.inv_dt_all[lo:hi],
-                               lvl.src_all[self._smooth][lo:hi], out, g=g, g_idx=g_idx,
-                               **self._host_dt(lvl.inv_dt_all_h[lo:hi]))
+        try:
+            self.problem.phi_batch(lvl.s, U, lvl.inv_dt_all[lo:hi],
+                                   lvl.src_all[self._smooth][lo:hi], out, g=g, g_idx=g_idx,
+                                   **self._host_dt(lvl.inv_dt_all_h[lo:hi]))
+        except NewtonConvergenceError as e:
+            col = getattr(e, "column", -1)
+            if 0 <= col < hi - lo:
+                e.at_time(lvl.t[lo + col], lvl.s)
+            raise
         self.phi_columns += hi - lo
         self.phi_calls += 1
 

@@ -179,7 +179,11 @@ class GpuFemProblem:
         if guess is not None and guess is not u_prev:
             gs = guess.field.to(self.device).reshape(1, n).contiguous()
         out = torch.empty(1, n, dtype=torch.float64, device=self.device)
-        self.phi_batch(spatial_level, u_in, inv_dt, src, out, guess=gs)
+        try:
+            self.phi_batch(spatial_level, u_in, inv_dt, src, out, guess=gs)
+        except NewtonConvergenceError as e:
+            e.at_time(t_next, spatial_level)
+            raise
         st = self.last_stats()
         if st["failed"]:
             raise PintGpuError(f"inner PCG did not converge at t={t_next:.6g} "
@@ -209,7 +213,12 @@ class GpuFemProblem:
             col, its = ctypes.c_int(), ctypes.c_int()
             self.lib.pg_newton_failure(self.ctx, ctypes.byref(col), ctypes.byref(its))
             msg = self.lib.pg_last_error(self.ctx).decode()
-            raise NewtonConvergenceError(msg, time=None, iterations=its.value)
+            # time = t_next of the failing column (reference problems.py:240-244):
+            # the batch only knows its columns, so callers that know the
+            # column's time (step(), the engine's sweeps) fill it in
+            err = NewtonConvergenceError(msg, time=None, iterations=its.value)
+            err.column = int(col.value)
+            raise err
         _lib.check(self.ctx, rc, "pg_phi_batch")
 
     def prefactor(self, level, inv_dt_host):

@@ -127,3 +127,44 @@ def test_newton_failure_is_recorded_not_raised(cuda):
     assert not run.converged
     assert run.failure is not None and "Newton" in run.failure
     assert sol is None
+
+
+def test_newton_failure_carries_time(cuda):
+    """NewtonConvergenceError.time = t_next of the failing step, as the
+    reference raises it (problems.py:240-244): through step() and through the
+    engine's batched sweeps."""
+    from paper_1912_03106_b200 import (BlockState, CycleSpec, GpuFemProblem, MgritSolver,
+                                       NewtonConvergenceError, StoppingCriterion,
+                                       TimeHierarchy, build_uniform_grid, configs)
+    spec = configs.config3(N=16, n_steps=64, levels=2, grids=1, strategy="none")
+    spec["nonlinear"]["newton"].update(max_iters=1, tol=1e-16)
+    gp = GpuFemProblem(spec)
+    n = gp.spatial.size(0)
+    u = BlockState(torch.zeros(n, dtype=torch.float64, device=gp.device))
+    with pytest.raises(NewtonConvergenceError) as ei:
+        gp.step(u, 0.001, 0.0015, 0)
+    assert ei.value.time == pytest.approx(0.0015)
+    assert "t=0.0015" in str(ei.value)
+    grid = build_uniform_grid(0.0, 0.02 * 8 / 1024, 8)
+    solver = MgritSolver(gp, TimeHierarchy.build(grid, [2]), CycleSpec(kind="V", max_iters=3),
+                         StoppingCriterion())
+    with pytest.raises(NewtonConvergenceError) as ei:
+        solver._phi_off(solver.levels[0], solver.levels[0].c_store, 1, solver.levels[0].w[0])
+    assert ei.value.time is not None and ei.value.time in set(float(t) for t in grid.points)
+
+
+def test_pcg_max_iters_is_an_error(cuda):
+    """An unconverged Jacobi-PCG Phi is refused (PG_ENOCONV ->
+    InnerSolveError), never handed to the engine as a result."""
+    from paper_1912_03106_b200 import GpuFemProblem, InnerSolveError, configs
+    spec = configs.config5(N=32)
+    spec["inner"]["max_iters"] = 3
+    prob = GpuFemProblem(spec, inner="pcg")
+    n = prob.spatial.size(0)
+    B = 4
+    U = torch.randn(B, n, dtype=torch.float64, device=prob.device)
+    out = torch.empty_like(U)
+    with pytest.raises(InnerSolveError):
+        prob.phi_batch(0, U, torch.full((B,), 1.0 / spec["dt"], dtype=torch.float64,
+                                        device=prob.device),
+                       torch.zeros(B, 0, dtype=torch.float64, device=prob.device), out)

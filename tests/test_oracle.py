@@ -194,3 +194,26 @@ def test_time_hierarchy_matches_reference_semantics():
     assert h.grids[1].n_points == 65
     assert np.array_equal(h.grids[1].points, g.points[::16])       # bitwise
     assert h.splittings[1].factor == 16 and h.splittings[1].n_intervals == 4
+
+
+def test_oracle_jacobi_pcg_matches_direct_solve():
+    """oracle/pcg.py (config 5's Jacobi-PCG, checker for the GPU's) on a
+    small config-5 operator: residual meets the stopping rule, the iterate is
+    within kappa * rtol of the direct solve, and a tighter rtol converges to it."""
+    import scipy.sparse.linalg as spla
+    from oracle import fem2d
+    from oracle.pcg import jacobi_pcg
+    from paper_1912_03106_b200 import configs
+    spec = configs.config5(N=32)
+    lv = fem2d.make_problem(spec).levels[0]
+    A = (lv.K + lv.M * (1.0 / spec["dt"])).tocsr()
+    U = np.random.default_rng(0).standard_normal((4, A.shape[0]))
+    rhs = (1.0 / spec["dt"]) * (lv.M @ U.T).T
+    exp = spla.splu(A.tocsc()).solve(rhs.T).T
+    for rtol, tol in ((1e-10, 1e-5), (1e-14, 1e-9)):
+        x, its = jacobi_pcg(A, rhs, U, rtol)
+        res = np.linalg.norm((A @ x.T).T - rhs, axis=1) / np.linalg.norm(rhs, axis=1)
+        assert res.max() < 1.05 * rtol + 1e-15
+        err = np.linalg.norm(x - exp, axis=1) / np.linalg.norm(exp, axis=1)
+        assert err.max() < tol, (rtol, err.max())
+        assert (its > 0).all()
