@@ -202,6 +202,14 @@ typedef struct pg_kernel_profile {
     double  alg_flops;
     int64_t column_iters;
 } pg_kernel_profile;
+/* Profiling (dev / bench): with profiling on every kernel of a Phi call is
+ * bracketed by CUDA events on the launching stream (and the call syncs).
+ * pg_profile_read fills up to n of the PG_PROFILE_KINDS entries, in order:
+ * k_sdir, k_supd (Jacobi-PCG), k_band_solve (= chains + SPIKE recombination),
+ * band_chain_fwd, band_chain_bwd, band_rhs, spike_border, spike_fix,
+ * band_scatter; alg_flops / alg_bytes are the algorithmic work (the
+ * reference's dpbtrs: 2 n w flops per direction and column). */
+#define PG_PROFILE_KINDS 9
 int  pg_profile(pg_ctx* ctx, int on);
 int  pg_profile_read(pg_ctx* ctx, pg_kernel_profile* out, int n, int reset);
 

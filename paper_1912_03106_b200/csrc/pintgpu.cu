@@ -108,6 +108,16 @@ struct Level {
 
 }  // namespace
 
+// profile kinds (pg_profile_read order).  k_band_solve is the sum of the
+// band-solve kinds (chains + SPIKE recombination) of a Phi call.
+enum {
+    PG_PROF_SDIR = 0, PG_PROF_SUPD, PG_PROF_BAND, PG_PROF_FWD, PG_PROF_BWD, PG_PROF_RHS,
+    PG_PROF_BORDER, PG_PROF_FIX, PG_PROF_SCATTER, PG_PROF_N
+};
+static const char* const PG_PROF_NAMES[PG_PROF_N] = {
+    "k_sdir", "k_supd", "k_band_solve", "band_chain_fwd", "band_chain_bwd", "band_rhs",
+    "spike_border", "spike_fix", "band_scatter"};
+
 struct pg_ctx {
     int device = 0;
     int n_sm = 148;
@@ -130,11 +140,11 @@ struct pg_ctx {
     bool prof_on = false;
     std::vector<cudaEvent_t> ev;         // pool: [2 per launch] within a poll chunk
     int ev_used = 0;
-    std::vector<int> ev_kind;            // 0 = k_sdir, 1 = k_supd
-    double prof_ms[3] = {0.0, 0.0, 0.0};
-    double prof_bytes[3] = {0.0, 0.0, 0.0};
-    double prof_flops[3] = {0.0, 0.0, 0.0};
-    int64_t prof_launches[3] = {0, 0, 0};
+    std::vector<int> ev_kind;            // PG_PROF_* kind of each (start, end) pair
+    double prof_ms[PG_PROF_N] = {};
+    double prof_bytes[PG_PROF_N] = {};
+    double prof_flops[PG_PROF_N] = {};
+    int64_t prof_launches[PG_PROF_N] = {};
     int64_t prof_cols = 0;
     unsigned long long prof_iters_seen = 0;
 };
@@ -1144,11 +1154,18 @@ static int spike_fix_gemm(pg_ctx* ctx, const Level::SpikePart& sp, bool fwd, con
 }
 
 template <int BCM>
+static int spike_fix(pg_ctx* ctx, const Level& L, const Level::SpikePart& sp, bool fwd,
+                     const SpikeArgs& a, int nch, const std::vector<int4>& hch,
+                     cudaStream_t st);
+
+template <int BCM>
 static int spike_recombine(pg_ctx* ctx, const Level& L, const Level::SpikePart& sp, bool fwd,
                            const SpikeArgs& a, int nch,
                            const std::vector<int4>& hch, cudaStream_t st) {
     const size_t sm = (size_t)L.bwin * BCM * sizeof(double);
     const size_t smb = sm + (size_t)1024 * BCM * sizeof(double);   // + red[S][BCM][W]
+    int rc;
+    if ((rc = prof_mark(ctx, PG_PROF_BORDER, st))) return rc;
     switch (L.bwin) {
 #define PG_BORDER(W_)                                                                      \
     case W_: {                                                                             \
@@ -1169,6 +1186,18 @@ static int spike_recombine(pg_ctx* ctx, const Level& L, const Level::SpikePart& 
         default: return set_err(ctx, PG_EINVAL, "spike window %d not supported", L.bwin);
     }
     LAUNCHED();
+    if ((rc = prof_mark(ctx, PG_PROF_BORDER, st))) return rc;
+    if ((rc = prof_mark(ctx, PG_PROF_FIX, st))) return rc;
+    rc = spike_fix<BCM>(ctx, L, sp, fwd, a, nch, hch, st);
+    if (rc) return rc;
+    return prof_mark(ctx, PG_PROF_FIX, st);
+}
+
+template <int BCM>
+static int spike_fix(pg_ctx* ctx, const Level& L, const Level::SpikePart& sp, bool fwd,
+                     const SpikeArgs& a, int nch, const std::vector<int4>& hch,
+                     cudaStream_t st) {
+    const size_t sm = (size_t)L.bwin * BCM * sizeof(double);
     // one GEMM per factor pays off for few, wide factor groups; many narrow
     // groups (bitwise-distinct dt of one level) go through one fused launch
     // (the fused launch re-reads a factor's G rows once per 8-column chunk: wide
@@ -1340,6 +1369,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     const bool fuse = BC >= 8 && ((band_rb_on() && (L.bwin > 256 || BC >= 16)) ||
                                   band_rb_on() == 2 || (L.bwin <= 256 && (ksv == 2 || ksv == 4))) &&
                       env_flag("PG_BAND_FUSE", 1);
+    if ((rc = prof_mark(ctx, PG_PROF_RHS, st))) return rc;
     if (L.dia && !copy_src && L.n_src <= BD_RHS_SRC && L.U <= 4 && env_flag("PG_RHS_DIA", 1)) {
         RhsDia ra{L.n, L.np, B, L.U, L.n_src, {0, 0, 0, 0, 0}, L.mk, L.shapes};
         for (int u = 1; u <= L.U; ++u) ra.off[u] = L.off[u];
@@ -1369,6 +1399,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
                                        L.shapes, u_prev, inv_dt, src, d_perm, L.Y, copy_src);
     }
     LAUNCHED();
+    if ((rc = prof_mark(ctx, PG_PROF_RHS, st))) return rc;
     // finest partition (8, 4, 2 chunks) whose chunk CTAs fit one wave; none:
     // the plain chains (the column groups already cover the SMs)
     int pi = -1;
@@ -1402,11 +1433,13 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     }
     const size_t sm = band_solve_smem(L, BC);
     SpikeArgs spa{L.bwin, spp.q, P, L.nblk, L.np, B, L.Y, d_chunks, spp.d_GF, L.spk_T};
-    if ((rc = prof_mark(ctx, 2, st))) return rc;
     for (int dir = 0; dir < 2 && !rc; ++dir) {
         const bool fwd = dir == 0;
         sa.F = fwd ? L.d_FL : L.d_FU;
+        const int pk = fwd ? PG_PROF_FWD : PG_PROF_BWD;
+        if ((rc = prof_mark(ctx, pk, st))) break;
         if ((rc = band_dir(ctx, L, BC, fwd, sa, dim3(nch, P), sm, st))) break;
+        if ((rc = prof_mark(ctx, pk, st))) break;
         if (spike) {
             spa.G = fwd ? spp.d_GF : spp.d_GB;
             rc = BC == 1 ? spike_recombine<1>(ctx, L, spp, fwd, spa, nch, grp->hch, st)
@@ -1414,31 +1447,44 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         }
     }
     if (rc) return rc;
-    if ((rc = prof_mark(ctx, 2, st))) return rc;
+    if (!(fuse && P == 1)) {
+        if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
+        dim3 gs(std::max(1, std::min(32, (L.n + 255) / 256)), B);
+        k_band_scatter<<<gs, 256, 0, st>>>(L.n, L.np, L.Y, d_perm, u_out, g, g_idx);
+        LAUNCHED();
+        if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
+    }
     if (ctx->prof_on) {
-        // algorithmic work of the forward + backward solves: per column
-        // 2 * 2 * np * (W + nb) flops; HBM bytes = Y in/out twice + each
-        // distinct factor pair read once
+        // algorithmic work (the reference's dpbtrs: 2 n w flops per direction
+        // and column, w = the lower bandwidth); HBM bytes of the chains: Y in
+        // and out + each distinct factor of the call read once
         std::vector<char> used(L.FL.size(), 0);
         for (const int4& q : grp->hch) used[q.x] = 1;
         double fb = 0.0;
-        for (char u : used) fb += u ? 2.0 * bd_block_doubles(L.bwin) * L.nblk * 8.0 : 0.0;
-        ctx->prof_flops[2] += 4.0 * L.np * (double)(L.bwin + BD_NB) * B;
-        ctx->prof_bytes[2] += 32.0 * L.np * B + fb;
+        for (char u : used) fb += u ? bd_block_doubles(L.bwin) * L.nblk * 8.0 : 0.0;
+        const double Bd = B;
+        for (int k : {PG_PROF_FWD, PG_PROF_BWD}) {
+            ctx->prof_flops[k] += 2.0 * L.n * (double)L.bw * Bd;
+            ctx->prof_bytes[k] += 16.0 * L.np * Bd + fb;
+        }
+        ctx->prof_bytes[PG_PROF_RHS] += 8.0 * (L.n + L.np) * Bd;
+        if (spike) {
+            const double fixed_rows = (double)L.np - (double)spp.q * BD_NB;   // chunks 1.. / ..P-2
+            ctx->prof_flops[PG_PROF_BORDER] += 2.0 * 2.0 * (P - 2) * (double)L.bwin * L.bwin * Bd;
+            ctx->prof_flops[PG_PROF_FIX] += 2.0 * 2.0 * fixed_rows * L.bwin * Bd;
+            ctx->prof_bytes[PG_PROF_FIX] += 2.0 * (16.0 * fixed_rows * Bd);
+        }
+        if (!(fuse && P == 1)) ctx->prof_bytes[PG_PROF_SCATTER] += 16.0 * L.n * Bd;
         CU(cudaStreamSynchronize(st));
         for (int k = 0; k + 1 < ctx->ev_used; k += 2) {
             float ms = 0.f;
             CU(cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]));
             ctx->prof_ms[ctx->ev_kind[k]] += ms;
-            ctx->prof_launches[ctx->ev_kind[k]] += 2;
+            ctx->prof_launches[ctx->ev_kind[k]] += 1;
         }
         ctx->ev_used = 0;
         ctx->ev_kind.clear();
     }
-    if (fuse && P == 1) return PG_OK;            // the backward chain wrote u_out
-    dim3 gs(std::max(1, std::min(32, (L.n + 255) / 256)), B);
-    k_band_scatter<<<gs, 256, 0, st>>>(L.n, L.np, L.Y, d_perm, u_out, g, g_idx);
-    LAUNCHED();
     return PG_OK;
 }
 
@@ -1673,17 +1719,28 @@ extern "C" int pg_profile(pg_ctx* ctx, int on) {
 
 extern "C" int pg_profile_read(pg_ctx* ctx, pg_kernel_profile* out, int n, int reset) {
     if (!ctx || !out || n < 2) return PG_EINVAL;
-    const char* names[3] = {"k_sdir", "k_supd", "k_band_solve"};
-    for (int k = 0; k < std::min(n, 3); ++k) {
-        snprintf(out[k].name, sizeof out[k].name, "%s", names[k]);
+    for (int k = 0; k < std::min(n, (int)PG_PROF_N); ++k) {
+        snprintf(out[k].name, sizeof out[k].name, "%s", PG_PROF_NAMES[k]);
         out[k].total_ms = ctx->prof_ms[k];
         out[k].launches = ctx->prof_launches[k];
         out[k].alg_bytes = ctx->prof_bytes[k];
         out[k].alg_flops = ctx->prof_flops[k];
         out[k].column_iters = ctx->prof_cols;
     }
+    if (n > PG_PROF_BAND) {
+        // the band-solve region = chains + SPIKE recombination
+        pg_kernel_profile& b = out[PG_PROF_BAND];
+        b.total_ms = b.alg_bytes = b.alg_flops = 0.0;
+        b.launches = 0;
+        for (int k : {PG_PROF_FWD, PG_PROF_BWD, PG_PROF_BORDER, PG_PROF_FIX}) {
+            b.total_ms += ctx->prof_ms[k];
+            b.launches += ctx->prof_launches[k];
+            b.alg_flops += ctx->prof_flops[k];
+            if (k == PG_PROF_FWD || k == PG_PROF_BWD) b.alg_bytes += ctx->prof_bytes[k];
+        }
+    }
     if (reset) {
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < PG_PROF_N; ++k) {
             ctx->prof_ms[k] = ctx->prof_bytes[k] = ctx->prof_flops[k] = 0.0;
             ctx->prof_launches[k] = 0;
         }

@@ -244,8 +244,9 @@ class GpuFemProblem:
         _lib.check(self.ctx, self.lib.pg_profile(self.ctx, int(bool(on))), "pg_profile")
 
     def profile_read(self, reset=False):
-        arr = (_lib.KernelProfile * 3)()
-        _lib.check(self.ctx, self.lib.pg_profile_read(self.ctx, arr, 3, int(reset)),
+        arr = (_lib.KernelProfile * _lib.PG_PROFILE_KINDS)()
+        _lib.check(self.ctx, self.lib.pg_profile_read(self.ctx, arr, _lib.PG_PROFILE_KINDS,
+                                                      int(reset)),
                    "pg_profile_read")
         return [dict(name=a.name.decode(), total_ms=a.total_ms, launches=int(a.launches),
                      alg_bytes=a.alg_bytes, alg_flops=a.alg_flops,
