@@ -1,5 +1,5 @@
-# full GPU tests + per-config breakdown (dev)
+# full GPU tests + smoke + default bench (dev)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/probe_breakdown.py cfg4 merge > gpurun_out/bd_cfg4.txt 2>&1
-timeout 300 python tools/probe_breakdown.py cfg2 > gpurun_out/bd_cfg2.txt 2>&1
+( time timeout 1500 python -m pytest tests -m gpu -x -q --durations=15 ) > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+( time timeout 1500 python bench.py ) > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
