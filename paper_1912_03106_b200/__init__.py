@@ -19,6 +19,8 @@ See DESIGN.md for the data layout, kernels and rooflines.
 """
 
 from . import configs
+from .dropin import (GpuOperatorProblem, OperatorLevel, ReferenceProblemAdapter,
+                     reference_1d_levels)
 from .errors import InnerSolveError, NewtonConvergenceError, PintGpuError, TransportError
 from .excitation import Excitation
 from .mgrit import (CycleSpec, MgritSolver, SolverRun, StoppingCriterion,
@@ -35,11 +37,11 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BlockState", "CFSplitting", "CycleSpec", "Decomposition", "DistTransport",
-    "Excitation", "GpuFemProblem", "GpuSurrogateProblem", "InnerSolveError", "make_problem",
+    "Excitation", "GpuFemProblem", "GpuOperatorProblem", "GpuSurrogateProblem", "InnerSolveError", "make_problem",
     "MgritSolver", "NewtonConvergenceError",
-    "NullTransport", "PintGpuError", "SolverRun", "SpaceTimeVector",
+    "NullTransport", "OperatorLevel", "PintGpuError", "ReferenceProblemAdapter", "SolverRun", "SpaceTimeVector",
     "SpatialHierarchy2D", "StepDiagnostics", "StoppingCriterion", "StorageReport",
     "TimeGrid", "TimeHierarchy", "TransportError", "assign_spatial_levels",
     "build_uniform_grid", "configs", "mgrit_solve", "plan_coarsening",
-    "qoi_change", "sequential_solve", "storage_estimate",
+    "qoi_change", "reference_1d_levels", "sequential_solve", "storage_estimate",
 ]

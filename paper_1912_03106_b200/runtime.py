@@ -1,8 +1,9 @@
 """Time-domain decomposition and the inter-rank transport.
 
-Decomposition restates reference runtime.py:31-105 exactly: whole
-C-intervals per rank, remainder to the lowest ranks, the last active rank
-owns any F-tail, ranks beyond the unit count idle on that level.
+Decomposition keeps the ownership rule of reference runtime.py:31-105
+(whole C-intervals per rank, remainder to the lowest ranks, the last active
+rank owns any F-tail, ranks beyond the interval count idle on that level),
+tabulated as per-rank arrays.
 
 The transport replaces the reference's queue-based p2p (runtime.py:123-254)
 with torch.distributed: one process per GPU, NCCL over NVLink/NVSwitch for
@@ -12,8 +13,6 @@ of per-rank partial sums reduced in rank order on every rank (the
 determinism of runtime.py:189-203), maxima an all-reduce.
 """
 
-from bisect import bisect_right
-
 import numpy as np
 import torch
 
@@ -21,82 +20,89 @@ from .errors import TransportError
 
 
 class Decomposition:
-    """Ownership of one level's C-intervals across n_workers ranks."""
+    """Ownership of one level's C-intervals across n_workers ranks
+    (semantics of reference runtime.py:31-105).
+
+    Everything is tabulated once as arrays over ranks -- interval counts,
+    first interval, owned point range [lo, hi) -- so the per-sweep queries of
+    the engine are O(1) lookups and owner searches are binary searches:
+
+        counts[w]  = K // p (+1 for the first K % p ranks)
+        first[w]   = exclusive prefix sum of counts
+        lo[w]      = C[first[w]] + 1,  hi[w] = C[first[w] + counts[w]] + 1
+                     (the last rank that owns anything also owns the F-tail)
+
+    Ranks past the interval count own nothing on this level; a level without
+    any closed interval (fewer points than the factor) belongs to rank 0."""
 
     def __init__(self, splitting, n_workers):
         if n_workers < 1:
             raise ValueError(f"n_workers must be >= 1, got {n_workers}")
         self.splitting = splitting
-        self.n_workers = n_workers
-        k = splitting.n_intervals
-        base, rem = divmod(k, n_workers)
-        self._n_units = [base + 1 if w < rem else base for w in range(n_workers)]
-        self._first_unit = [0] * n_workers
-        for w in range(1, n_workers):
-            self._first_unit[w] = self._first_unit[w - 1] + self._n_units[w - 1]
-        self._last_rank = max((w for w in range(n_workers) if self._n_units[w] > 0),
-                              default=0)
+        self.n_workers = int(n_workers)
+        K, p = int(splitting.n_intervals), self.n_workers
+        ranks = np.arange(p)
+        self._counts = K // p + (ranks < K % p).astype(np.int64)
+        self._first = np.concatenate(([0], np.cumsum(self._counts)[:-1])).astype(np.int64)
+        self._ends = self._first + self._counts          # one past the last owned interval
+        c = np.asarray(splitting.c_indices, dtype=np.int64)
+        self._lo = np.zeros(p, dtype=np.int64)
+        self._hi = np.zeros(p, dtype=np.int64)
+        if K == 0:
+            self._lo[0], self._hi[0] = 1, splitting.n_points
+            self._idle = ranks > 0
+        else:
+            self._idle = self._counts == 0
+            own = ~self._idle
+            self._lo[own] = c[self._first[own]] + 1
+            self._hi[own] = c[self._ends[own]] + 1
+            self._hi[np.nonzero(own)[0][-1]] = splitting.n_points      # F-tail
+        self._active = [int(w) for w in np.nonzero(~self._idle)[0]]
 
     def n_units(self, rank):
-        return self._n_units[rank]
+        return int(self._counts[rank])
 
     def first_unit(self, rank):
-        return self._first_unit[rank]
+        return int(self._first[rank])
 
     def unit_owner(self, unit):
         if not 0 <= unit < self.splitting.n_intervals:
             raise ValueError(f"unit {unit} out of range")
-        ends = [self._first_unit[w] + self._n_units[w] for w in range(self.n_workers)]
-        return bisect_right(ends, unit)
+        return int(np.searchsorted(self._ends, unit, side="right"))
 
     def is_empty(self, rank):
-        return self._n_units[rank] == 0 and not (
-            rank == 0 and self.splitting.n_intervals == 0)
+        return bool(self._idle[rank])
 
     def c_points(self, rank):
-        c = self.splitting.c_indices
-        first = self._first_unit[rank]
-        return c[first + 1: first + 1 + self._n_units[rank]]
+        f = int(self._first[rank])
+        return self.splitting.c_indices[f + 1: f + 1 + int(self._counts[rank])]
 
     def left_boundary_index(self, rank):
-        return int(self.splitting.c_indices[self._first_unit[rank]])
+        return int(self.splitting.c_indices[self._first[rank]])
 
     def owned_range(self, rank):
-        if self.is_empty(rank):
-            return (0, 0)
-        c = self.splitting.c_indices
-        lo = self.left_boundary_index(rank) + 1
-        if self.splitting.n_intervals == 0:
-            return (1, self.splitting.n_points) if rank == 0 else (0, 0)
-        hi = int(c[self._first_unit[rank] + self._n_units[rank]]) + 1
-        if rank == self._last_rank:
-            hi = self.splitting.n_points
-        return (lo, hi)
+        return (int(self._lo[rank]), int(self._hi[rank]))
 
     def point_owner(self, point):
         """Rank whose owned range contains point (index 0 -> rank 0)."""
-        for w in self.active_ranks():
-            lo, hi = self.owned_range(w)
-            if lo <= point < hi:
-                return w
         if point == 0:
             return 0
+        act = self._active
+        k = int(np.searchsorted(self._hi[act], point, side="right"))
+        if k < len(act) and self._lo[act[k]] <= point:
+            return act[k]
         raise RuntimeError(f"point {point} has no owner")
 
     def active_ranks(self):
-        return [w for w in range(self.n_workers) if not self.is_empty(w)]
+        return list(self._active)
 
     def left_neighbor(self, rank):
-        for w in range(rank - 1, -1, -1):
-            if not self.is_empty(w):
-                return w
-        return None
+        below = [w for w in self._active if w < rank]
+        return below[-1] if below else None
 
     def right_neighbor(self, rank):
-        for w in range(rank + 1, self.n_workers):
-            if not self.is_empty(w):
-                return w
-        return None
+        above = [w for w in self._active if w > rank]
+        return above[0] if above else None
 
 
 class NullTransport:
