@@ -17,8 +17,8 @@ OUT = os.path.join(HERE, "lib", "libpintgpu.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
          "-Xptxas", "-warn-spills"]
-# cuBLAS only for the plain rank-W GEMM of the SPIKE correction
-LIBS = ["-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+# no library kernels: the CUDA runtime is the only dependency
+LIBS = ["-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 
 
 def sources():

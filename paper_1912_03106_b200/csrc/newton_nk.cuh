@@ -1,10 +1,14 @@
 // Batched Newton-Krylov for the nonlinear model (inner = banded Cholesky).
 //
-// Host-driven version of the reference's damped Newton (problems.py:201-244)
-// over masked column sets (one column per C-interval): every step is a
-// batched kernel over the active columns, every decision (converged?
-// halve?) is the reference's per-column rule taken on the host from the
-// per-column norms.  The Newton system J(u) d = -F is solved by CG
+// The reference's damped Newton (problems.py:201-244) over masked column
+// sets (one column per C-interval): every step is a batched kernel over the
+// active columns.  The Newton-level decisions (converged? halve?) are the
+// reference's per-column rules taken on the host from per-column norms (a few
+// reads per Phi call); the inner CG keeps its per-column convergence flags on
+// the device (k_nk_cg_a sets flag bit 0 when |r| <= rtol |F|, every CG kernel
+// skips flagged columns), so the host launches bursts of iterations and only
+// reads the flags between bursts to re-pack the active list.
+// The Newton system J(u) d = -F is solved by CG
 // preconditioned with the banded-Cholesky factor of the linearised operator
 // c M + K(nu_iron(0)) -- one per distinct dt, shared with the band-solve
 // machinery (band.cuh) -- so the inner solve takes a handful of iterations
@@ -129,9 +133,11 @@ k_nk_residual(NkLevel L, const int* __restrict__ act, const double* __restrict__
 
 // Q = J(u) P over active columns                 grid (row chunks, active)
 __global__ void k_nk_japply(NkLevel L, const int* __restrict__ act,
+                            const int* __restrict__ flag,
                             const double* __restrict__ inv_dt, const double* __restrict__ P,
                             const double* __restrict__ E, double* __restrict__ Q) {
     const int b = act[blockIdx.y];
+    if (flag[b] & 1) return;                       // CG of this column has converged
     const size_t off = (size_t)b * L.n;
     const double c = inv_dt[b];
     const double* p = P + off;
@@ -166,9 +172,11 @@ __global__ void k_nk_japply(NkLevel L, const int* __restrict__ act,
 }
 
 // r = -F, d = 0                                   grid (row chunks, active)
-__global__ void k_nk_start(int n, const int* __restrict__ act, const double* __restrict__ F,
+__global__ void k_nk_start(int n, const int* __restrict__ act, int* __restrict__ flag,
+                           const double* __restrict__ F,
                            double* __restrict__ R, double* __restrict__ D) {
     const size_t off = (size_t)act[blockIdx.y] * n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) flag[act[blockIdx.y]] = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         R[off + i] = -F[off + i];
         D[off + i] = 0.0;
@@ -177,11 +185,14 @@ __global__ void k_nk_start(int n, const int* __restrict__ act, const double* __r
 
 // alpha = rho / p.q ; d += alpha p ; r -= alpha q ; rr = |r|^2   (CTA per column)
 __global__ void __launch_bounds__(NK_NT)
-k_nk_cg_a(int n, const int* __restrict__ act, const double* __restrict__ P,
+k_nk_cg_a(int n, const int* __restrict__ act, int* __restrict__ flag,
+          const double* __restrict__ P,
           const double* __restrict__ Q, double* __restrict__ D, double* __restrict__ R,
-          const double* __restrict__ rho, double* __restrict__ rr) {
+          const double* __restrict__ rho, double* __restrict__ rr,
+          const double* __restrict__ f2, double rtol) {
     __shared__ double red[2 * (NK_NT / 32) + 2];
     const int b = act[blockIdx.x];
+    if (flag[b] & 1) return;
     const size_t off = (size_t)b * n;
     double acc = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) acc = fma(P[off + i], Q[off + i], acc);
@@ -195,16 +206,23 @@ k_nk_cg_a(int n, const int* __restrict__ act, const double* __restrict__ P,
         acc = fma(r, r, acc);
     }
     const double s = nk_sum(acc, red);
-    if (threadIdx.x == 0) rr[b] = s;
+    if (threadIdx.x == 0) {
+        rr[b] = s;
+        // converged when |r| <= rtol |F(u)| (the host rule: rr > stop^2 continues)
+        const double stop = rtol * sqrt(f2[b]);
+        if (!(s > stop * stop)) flag[b] = 1;
+    }
 }
 
 // rz = r.z ; beta = rz / rho (0 on the first) ; rho = rz ; p = z + beta p
 __global__ void __launch_bounds__(NK_NT)
-k_nk_cg_b(int n, const int* __restrict__ act, const double* __restrict__ R,
+k_nk_cg_b(int n, const int* __restrict__ act, const int* __restrict__ flag,
+          const double* __restrict__ R,
           const double* __restrict__ Z, double* __restrict__ P, double* __restrict__ rho,
           int first) {
     __shared__ double red[2 * (NK_NT / 32) + 2];
     const int b = act[blockIdx.x];
+    if (flag[b] & 1) return;
     const size_t off = (size_t)b * n;
     // read rho before the reduction's barriers: thread 0 overwrites it below
     const double rho_old = rho[b];
@@ -232,8 +250,10 @@ __global__ void k_nk_trial(int n, const int* __restrict__ act, const double* __r
 __global__ void k_nk_accept(int n, int n_elem, const int* __restrict__ act,
                             const double* __restrict__ TR, const double* __restrict__ FT,
                             const double* __restrict__ ET, double* __restrict__ U,
-                            double* __restrict__ F, double* __restrict__ E) {
+                            double* __restrict__ F, double* __restrict__ E,
+                            const double* __restrict__ t2, double* __restrict__ f2) {
     const int b = act[blockIdx.y];
+    if (blockIdx.x == 0 && threadIdx.x == 0) f2[b] = t2[b];       // |F(u)|^2 of the accepted iterate
     const size_t off = (size_t)b * n, eoff = (size_t)b * n_elem * 4;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         U[off + i] = TR[off + i];

@@ -9,6 +9,7 @@
 #include "newton.cuh"
 #include "band.cuh"
 #include "band_rb.cuh"
+#include "spike_gemm.cuh"
 #include "newton_nk.cuh"
 
 #include <algorithm>
@@ -18,7 +19,6 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
-#include <cublas_v2.h>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -84,13 +84,18 @@ struct Level {
     double* spk_T = nullptr;                // [P][W][B] border values
     size_t spk_T_cap = 0;
     int4* d_spk_chunks = nullptr;           // spike generation column groups
+    int4* d_gtiles = nullptr;               // column tiles of the correction GEMM
+    int gt_cap = 0;
     // batched Newton-Krylov workspace
     double *nk_u = nullptr, *nk_F = nullptr, *nk_D = nullptr, *nk_rhs = nullptr,
            *nk_R = nullptr, *nk_Z = nullptr, *nk_P = nullptr, *nk_Q = nullptr,
            *nk_TR = nullptr, *nk_FT = nullptr, *nk_E = nullptr, *nk_ET = nullptr,
            *nk_s = nullptr;          // per-column scalars [6][B]
     int* nk_act = nullptr;
+    int* nk_flag = nullptr;         // per column: bit 0 = inner CG converged
     int nk_B = 0;
+    std::vector<int> tmp_sub;      // column subset tmp_group was built for
+    int tmp_BC = 0;
     int* d_status = nullptr;
     // nonlinear iron elements
     int n_elem = 0;
@@ -121,7 +126,6 @@ static const char* const PG_PROF_NAMES[PG_PROF_N] = {
 struct pg_ctx {
     int device = 0;
     int n_sm = 148;
-    cublasHandle_t cublas = nullptr;      // SPIKE correction GEMMs (lazy)
     int64_t host_iters_last = 0, host_iters_total = 0;   // host-driven (Newton-Krylov) CG iterations
     bool dev_stats_last = false;          // last call used the device counters
     std::vector<Level> levels;
@@ -134,6 +138,17 @@ struct pg_ctx {
     unsigned long long* d_iters = nullptr;  // [0] cumulative, [1] this call
     int* d_ictr = nullptr;                  // [0] max iters this call, [1] failed cumulative, [2] failed this call
     int* h_poll = nullptr;        // pinned
+    // pinned staging for small host->device lists (active columns, column
+    // groupings) and device->host reads: pageable cudaMemcpyAsync would
+    // synchronise with the stream on every call
+    static constexpr int PIN_SLOTS = 32;
+    char* pin_base = nullptr;
+    size_t pin_slot = 0;
+    int pin_next = 0;
+    cudaEvent_t pin_ev[PIN_SLOTS] = {};
+    bool pin_busy[PIN_SLOTS] = {};
+    char* pin_fetch = nullptr;
+    size_t pin_fetch_cap = 0;
     int last_level = -1;
     int newton_fail_col = -1, newton_fail_iters = 0;
     // kernel profiling (CUDA events around every streamed-PCG launch)
@@ -190,6 +205,49 @@ static int set_err(pg_ctx* ctx, int code, const char* fmt, ...) {
             done_.fetch_or(bit_, std::memory_order_release);                               \
         }                                                                                  \
     } while (0)
+
+// stream-ordered upload of a small host array through the pinned ring: the
+// source may be reused as soon as the call returns, nothing synchronises
+// unless all slots are still in flight
+static int pin_upload(pg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!bytes) return PG_OK;
+    if (bytes > ctx->pin_slot) {
+        CU(cudaStreamSynchronize(st));
+        for (int i = 0; i < pg_ctx::PIN_SLOTS; ++i)
+            if (ctx->pin_busy[i]) {
+                CU(cudaEventSynchronize(ctx->pin_ev[i]));
+                ctx->pin_busy[i] = false;
+            }
+        if (ctx->pin_base) cudaFreeHost(ctx->pin_base);
+        ctx->pin_base = nullptr;
+        ctx->pin_slot = std::max<size_t>(2 * bytes, 64 * 1024);
+        CU(cudaMallocHost(&ctx->pin_base, ctx->pin_slot * pg_ctx::PIN_SLOTS));
+    }
+    const int sl = ctx->pin_next;
+    ctx->pin_next = (sl + 1) % pg_ctx::PIN_SLOTS;
+    if (!ctx->pin_ev[sl]) CU(cudaEventCreateWithFlags(&ctx->pin_ev[sl], cudaEventDisableTiming));
+    if (ctx->pin_busy[sl]) CU(cudaEventSynchronize(ctx->pin_ev[sl]));
+    char* h = ctx->pin_base + (size_t)sl * ctx->pin_slot;
+    memcpy(h, src, bytes);
+    CU(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(ctx->pin_ev[sl], st));
+    ctx->pin_busy[sl] = true;
+    return PG_OK;
+}
+
+// device -> host read of a small array (pinned bounce buffer; synchronises)
+static int pin_read(pg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes > ctx->pin_fetch_cap) {
+        if (ctx->pin_fetch) cudaFreeHost(ctx->pin_fetch);
+        ctx->pin_fetch = nullptr;
+        ctx->pin_fetch_cap = std::max<size_t>(2 * bytes, 64 * 1024);
+        CU(cudaMallocHost(&ctx->pin_fetch, ctx->pin_fetch_cap));
+    }
+    CU(cudaMemcpyAsync(ctx->pin_fetch, src, bytes, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    memcpy(dst, ctx->pin_fetch, bytes);
+    return PG_OK;
+}
 
 template <typename T>
 static int dev_upload(pg_ctx* ctx, T** dst, const T* src, size_t count) {
@@ -259,7 +317,7 @@ static void free_level(Level& L) {
     void* ptrs[] = {L.row_ptr, L.col_idx, L.m_val, L.k_val, L.dM, L.dK, L.shapes,
                     L.weights, L.tile_lo, L.tile_hi, L.elem_dof, L.elem_geo,
                     L.ne_ptr, L.ne, L.mk, L.a0, L.dinv0, L.cb0, L.d_FL, L.d_FU, L.Y, L.d_perm,
-                    L.d_chunks, L.d_status, L.k_pre, L.spk_T, L.d_spk_chunks};
+                    L.d_chunks, L.d_status, L.k_pre, L.spk_T, L.d_spk_chunks, L.d_gtiles};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : L.ws_allocs) cudaFree(p);
@@ -282,6 +340,7 @@ static void free_level(Level& L) {
     for (double* p : nk)
         if (p) cudaFree(p);
     if (L.nk_act) cudaFree(L.nk_act);
+    if (L.nk_flag) cudaFree(L.nk_flag);
 }
 
 extern "C" void pg_destroy(pg_ctx* ctx) {
@@ -289,10 +348,13 @@ extern "C" void pg_destroy(pg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     for (auto& L : ctx->levels) free_level(L);
-    if (ctx->cublas) cublasDestroy(ctx->cublas);
     cudaFree(ctx->d_iters);
     cudaFree(ctx->d_ictr);
     for (auto e : ctx->ev) cudaEventDestroy(e);
+    for (auto e : ctx->pin_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->pin_base) cudaFreeHost(ctx->pin_base);
+    if (ctx->pin_fetch) cudaFreeHost(ctx->pin_fetch);
     cudaFreeHost(ctx->h_poll);
     delete ctx;
 }
@@ -1109,57 +1171,44 @@ static int ensure_spikes(pg_ctx* ctx, Level& L, int pi, int f, cudaStream_t st) 
 }
 
 // y_p += G_p t_{p-1 / p+1} for every non-first chunk: a plain rank-W GEMM per
-// factor (columns [c0, c1) of the grouped batch), cuBLAS DGEMM (fp64 DMMA)
-static int spike_fix_gemm(pg_ctx* ctx, const Level::SpikePart& sp, bool fwd, const SpikeArgs& a,
+// factor over its columns of the grouped batch -- k_spike_gemm (spike_gemm.cuh,
+// fp64 DMMA tiles).  The column tiles (factor, first column, <= 64 columns) are
+// cut from the host copy of the column groups and go up through the pinned ring.
+static int spike_fix_gemm(pg_ctx* ctx, Level& L, bool fwd, const SpikeArgs& a,
                           const std::vector<int4>& hch, cudaStream_t st) {
-    if (!ctx->cublas && cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS)
-        return set_err(ctx, PG_ECUDA, "cublasCreate failed");
-    if (cublasSetStream(ctx->cublas, st) != CUBLAS_STATUS_SUCCESS)
-        return set_err(ctx, PG_ECUDA, "cublasSetStream failed");
-    const double one = 1.0;
-    const int W = a.W, P = a.P, ru = a.q * BD_NB;
-    const int rl = (a.nblk - (P - 1) * a.q) * BD_NB;         // last (longest) chunk
-    const long long sT = (long long)a.ldt * W;
-    const std::vector<double*>& G = fwd ? sp.GF : sp.GB;
+    std::vector<int4> tiles;
     for (size_t i = 0; i < hch.size();) {
         size_t j = i;
         while (j < hch.size() && hch[j].x == hch[i].x) ++j;
-        const double* Gf = G[hch[i].x];
         const int c0 = hch[i].y, nc = hch[j - 1].y + hch[j - 1].z - c0;
-        cublasStatus_t cs = CUBLAS_STATUS_SUCCESS;
-        if (fwd) {
-            // chunks 1 .. P-2 (uniform, border of p - 1), then the last
-            if (P > 2)
-                cs = cublasDgemmStridedBatched(
-                    ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ru, nc, W, &one, Gf + ru, a.ldy, ru,
-                    a.T + (size_t)c0 * W, W, sT, &one, a.Y + (size_t)c0 * a.ldy + ru, a.ldy, ru,
-                    P - 2);
-            if (cs == CUBLAS_STATUS_SUCCESS)
-                cs = cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, rl, nc, W, &one,
-                                 Gf + (size_t)(P - 1) * ru, a.ldy,
-                                 a.T + ((size_t)(P - 2) * a.ldt + c0) * W, W, &one,
-                                 a.Y + (size_t)c0 * a.ldy + (size_t)(P - 1) * ru, a.ldy);
-        } else {
-            // chunks 0 .. P-2 (uniform, border of p + 1)
-            cs = cublasDgemmStridedBatched(
-                ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ru, nc, W, &one, Gf, a.ldy, ru,
-                a.T + ((size_t)a.ldt + c0) * W, W, sT, &one, a.Y + (size_t)c0 * a.ldy, a.ldy, ru,
-                P - 1);
-        }
-        if (cs != CUBLAS_STATUS_SUCCESS)
-            return set_err(ctx, PG_ECUDA, "cuBLAS DGEMM failed (status %d)", (int)cs);
-        i = j;                 // (library launches: not counted as ours)
+        for (int c = 0; c < nc; c += SG_TN)
+            tiles.push_back(make_int4(hch[i].x, c0 + c, std::min(SG_TN, nc - c), 0));
+        i = j;
     }
+    if ((int)tiles.size() > L.gt_cap) {
+        if (L.d_gtiles) cudaFree(L.d_gtiles);
+        L.gt_cap = std::max<int>(2 * (int)tiles.size(), 64);
+        CU(cudaMalloc(&L.d_gtiles, L.gt_cap * sizeof(int4)));
+    }
+    int rc = pin_upload(ctx, L.d_gtiles, tiles.data(), tiles.size() * sizeof(int4), st);
+    if (rc) return rc;
+    const int rows = std::max(a.q, a.nblk - (a.P - 1) * a.q) * BD_NB;   // longest chunk
+    dim3 grid((rows + SG_TM - 1) / SG_TM, a.P - 1, (unsigned)tiles.size());
+    SMEM_ATTR_ONCE(k_spike_gemm<true>, SG_SMEM);
+    SMEM_ATTR_ONCE(k_spike_gemm<false>, SG_SMEM);
+    if (fwd) k_spike_gemm<true><<<grid, 256, SG_SMEM, st>>>(a, L.d_gtiles);
+    else k_spike_gemm<false><<<grid, 256, SG_SMEM, st>>>(a, L.d_gtiles);
+    LAUNCHED();
     return PG_OK;
 }
 
 template <int BCM>
-static int spike_fix(pg_ctx* ctx, const Level& L, const Level::SpikePart& sp, bool fwd,
+static int spike_fix(pg_ctx* ctx, Level& L, const Level::SpikePart& sp, bool fwd,
                      const SpikeArgs& a, int nch, const std::vector<int4>& hch,
                      cudaStream_t st);
 
 template <int BCM>
-static int spike_recombine(pg_ctx* ctx, const Level& L, const Level::SpikePart& sp, bool fwd,
+static int spike_recombine(pg_ctx* ctx, Level& L, const Level::SpikePart& sp, bool fwd,
                            const SpikeArgs& a, int nch,
                            const std::vector<int4>& hch, cudaStream_t st) {
     const size_t sm = (size_t)L.bwin * BCM * sizeof(double);
@@ -1194,22 +1243,21 @@ static int spike_recombine(pg_ctx* ctx, const Level& L, const Level::SpikePart& 
 }
 
 template <int BCM>
-static int spike_fix(pg_ctx* ctx, const Level& L, const Level::SpikePart& sp, bool fwd,
+static int spike_fix(pg_ctx* ctx, Level& L, const Level::SpikePart& sp, bool fwd,
                      const SpikeArgs& a, int nch, const std::vector<int4>& hch,
                      cudaStream_t st) {
     const size_t sm = (size_t)L.bwin * BCM * sizeof(double);
-    // one GEMM per factor pays off for few, wide factor groups; many narrow
-    // groups (bitwise-distinct dt of one level) go through one fused launch
-    // (the fused launch re-reads a factor's G rows once per 8-column chunk: wide
-    // groups -- >= 48 columns per factor on average -- go to the GEMMs, which
-    // tile G once; narrower ones are not worth ~2 small GEMM launches per factor)
+    // the tiled GEMM pays off for wide factor groups (>= 48 columns per factor
+    // on average: a 64-column tile reads its G rows once); many narrow groups
+    // (bitwise-distinct dt of one level) go through k_spike_fix, which re-reads
+    // G once per 8-column chunk but wastes no tensor work on empty columns
     int groups = 0, cols = 0;
     for (size_t i = 0; i < hch.size(); ++i) {
         groups += (i == 0 || hch[i].x != hch[i - 1].x);
         cols += hch[i].z;
     }
     if (BCM > 1 && (groups <= 2 || cols >= 48 * groups))
-        return spike_fix_gemm(ctx, sp, fwd, a, hch, st);
+        return spike_fix_gemm(ctx, L, fwd, a, hch, st);
     const int rows = std::max(a.q, a.nblk - (a.P - 1) * a.q) * BD_NB;  // longest chunk
     if (BCM == 1 && L.bwin % 8 == 0) {
         dim3 g1((rows + 31) / 32, a.P - 1, nch);
@@ -1306,11 +1354,15 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     // cached grouping for this exact inv_dt pattern?
     const uint64_t h = hash_doubles(c.data(), B);
     Level::Group* grp = nullptr;
-    if (!sub)
+    if (!sub) {
         for (auto& gr : L.groups[h])
             if ((int)gr.key.size() == B && gr.BC == BC &&
                 memcmp(gr.key.data(), c.data(), B * sizeof(double)) == 0)
                 grp = &gr;
+    } else if ((int)L.tmp_sub.size() == B && L.tmp_BC == BC &&
+               memcmp(L.tmp_sub.data(), sub, B * sizeof(int)) == 0) {
+        grp = &L.tmp_group;        // same subset as the previous call (a CG burst)
+    }
     int rc;
     std::vector<int> fid;
     if (!grp) {
@@ -1338,11 +1390,12 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
                 CU(cudaMalloc(&L.d_perm, L.perm_cap * sizeof(int)));
                 CU(cudaMalloc(&L.d_chunks, L.perm_cap * sizeof(int4)));
             }
-            CU(cudaMemcpyAsync(L.d_perm, perm.data(), B * sizeof(int), cudaMemcpyHostToDevice, st));
-            CU(cudaMemcpyAsync(L.d_chunks, chunks.data(), chunks.size() * sizeof(int4),
-                               cudaMemcpyHostToDevice, st));
-            CU(cudaStreamSynchronize(st));       // host vectors go out of scope
+            if ((rc = pin_upload(ctx, L.d_perm, perm.data(), B * sizeof(int), st))) return rc;
+            if ((rc = pin_upload(ctx, L.d_chunks, chunks.data(), chunks.size() * sizeof(int4), st)))
+                return rc;
             L.tmp_group = Level::Group{c, L.d_perm, L.d_chunks, (int)chunks.size(), BC, chunks};
+            L.tmp_sub.assign(sub, sub + B);
+            L.tmp_BC = BC;
             grp = &L.tmp_group;
         } else {
             Level::Group gr{c, nullptr, nullptr, (int)chunks.size(), BC, chunks};

@@ -130,6 +130,26 @@ class SolverRun:
         return self.setup_seconds + self.solve_seconds
 
 
+class _Boundary:
+    """Left-boundary state of a sweep whose exchange may still be in flight."""
+
+    __slots__ = ("buf", "pending")
+
+    def __init__(self, buf, pending):
+        self.buf, self.pending = buf, pending
+
+    def ready(self):
+        if self.pending is not None:
+            self.pending.wait()
+            self.pending = None
+        return self.buf
+
+
+def _drain(boundary):
+    if boundary is not None:
+        boundary.ready()
+
+
 class _Level:
     """Per-rank device workspace of one time level."""
 
@@ -293,23 +313,32 @@ class MgritSolver:
 
     # --- communication (reference mgrit.py:339-357) ---
     def _exchange_left(self, lvl):
+        """Send the last owned C-state (pre-sweep) right, receive the left
+        boundary (mgrit.py:339-350).  The transfer is in flight until the
+        returned boundary's ready(); _starts overlaps it with the
+        copy of the interior interval starts, the only work of a sweep that
+        does not depend on the boundary's batch."""
         d, r = lvl.decomp, self.transport.rank
         if lvl.empty:
             return None
         right, left = d.right_neighbor(r), d.left_neighbor(r)
         sends = [(right, lvl.c_store[-1])] if (right is not None and lvl.K) else []
         if left is None:
-            self.transport.exchange(sends, [])
-            return lvl.anchor
+            return _Boundary(lvl.anchor, self.transport.exchange_async(sends, []))
         buf = torch.empty(lvl.n, dtype=torch.float64, device=self.problem.device)
-        self.transport.exchange(sends, [(left, buf)])
-        return buf
+        return _Boundary(buf, self.transport.exchange_async(sends, [(left, buf)]))
 
     def _starts(self, lvl, boundary):
+        """Interval starts of a sweep: row 0 = the left boundary, row k = the
+        pre-sweep C-value k - 1.  The interior rows are copied while the
+        boundary exchange is still in flight."""
+        if boundary is None:
+            return lvl.start
+        if lvl.K > 1:
+            lvl.start[1:].copy_(lvl.c_store[:-1])
+        buf = boundary.ready()
         if lvl.K:
-            lvl.start[0].copy_(boundary)
-            if lvl.K > 1:
-                lvl.start[1:].copy_(lvl.c_store[:-1])
+            lvl.start[0].copy_(buf)
         return lvl.start
 
     def _walk(self, lvl, start):
@@ -340,6 +369,7 @@ class MgritSolver:
         self._probe_prop = None
         boundary = self._exchange_left(lvl)
         if lvl.empty or not lvl.K:
+            _drain(boundary)
             return
         last_f = self._walk(lvl, self._starts(lvl, boundary))
         self._phi_off(lvl, last_f, lvl.m, lvl.c_store)
@@ -380,6 +410,8 @@ class MgritSolver:
             j0 = lvl.first + 1
             self._phi_pts(nxt, lvl.lkept, j0, j0 + lvl.K, lvl.cprop)
             prob.fas_rhs(nxt.s, coarsen, lvl.kept, lvl.cprop, lvl.res, lvl.crhs)
+        else:
+            _drain(boundary)
         local, sends, recvs = self._restrict_plan(lvl, nxt)
         j0 = lvl.first + 1
         for _, lo, hi in local:
@@ -475,6 +507,8 @@ class MgritSolver:
         if not coarse.empty and not solved:
             boundary = self._exchange_left(coarse)
             m, K = coarse.m, coarse.K
+            if not K:
+                _drain(boundary)
             if K:
                 cur = self._starts(coarse, boundary)
                 for j in range(1, m + 1):
@@ -492,7 +526,7 @@ class MgritSolver:
             # F-tail after the last owned C-point (mgrit.py:529-532)
             last_c = int(coarse.c_idx[-1]) if K else coarse.left_index
             if coarse.own_hi - 1 > last_c:
-                v = (coarse.c_store[-1] if K else boundary).reshape(1, -1).contiguous()
+                v = (coarse.c_store[-1] if K else boundary.ready()).reshape(1, -1).contiguous()
                 for i in range(last_c + 1, coarse.own_hi):
                     out = torch.empty_like(v)
                     use_g = coarse.use_rhs
@@ -551,6 +585,7 @@ class MgritSolver:
         self._probe_prop = (False if (lvl.index == 0 and not self._smooth and not lvl.use_rhs)
                             else None)
         if lvl.empty or not lvl.K:
+            _drain(boundary)
             return 0.0, np.zeros(0)
         last_f = self._walk(lvl, self._starts(lvl, boundary))
         prop = self._other(lvl, last_f)
@@ -747,6 +782,8 @@ class MgritSolver:
             boundary = self._exchange_left(lvl)
             chunk = torch.empty(lvl.n_owned, lvl.n, dtype=torch.float64, device=dev)
             m, K = lvl.m, lvl.K
+            if not K:
+                _drain(boundary)
             if K:
                 cur = self._starts(lvl, boundary)
                 for j in range(1, m):
@@ -756,7 +793,7 @@ class MgritSolver:
                     cur = out
                 chunk[m - 1::m][:K].copy_(lvl.c_store)
             last_c = int(lvl.c_idx[-1]) if K else lvl.left_index
-            v = (lvl.c_store[-1] if K else boundary).reshape(1, -1).contiguous()
+            v = (lvl.c_store[-1] if K else boundary.ready()).reshape(1, -1).contiguous()
             for i in range(last_c + 1, lvl.own_hi):
                 out = torch.empty_like(v)
                 self._phi_pts(lvl, v, i, i + 1, out)

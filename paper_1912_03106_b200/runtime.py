@@ -105,6 +105,29 @@ class Decomposition:
         return above[0] if above else None
 
 
+class _Done:
+    """Handle of an exchange that has nothing left to wait for."""
+
+    def wait(self):
+        pass
+
+
+class _Pending:
+    """In-flight grouped p2p batch.  wait() orders the caller's stream after
+    the transfers (NCCL: a stream dependency, the host does not block) and
+    lands host-staged receives in their device buffers (gloo)."""
+
+    def __init__(self, reqs, staged):
+        self.reqs, self.staged = reqs, staged
+
+    def wait(self):
+        for req in self.reqs:
+            req.wait()
+        for _, h, t in self.staged:
+            t.copy_(h)
+        self.reqs, self.staged = [], []
+
+
 class NullTransport:
     """Single worker: no peers (reference runtime.py:110-120)."""
 
@@ -114,6 +137,10 @@ class NullTransport:
     def exchange(self, sends, recvs):
         if sends or recvs:
             raise TransportError("no peers in a single-worker run")
+
+    def exchange_async(self, sends, recvs):
+        self.exchange(sends, recvs)
+        return _Done()
 
     def sum_ordered(self, value):
         return float(value)
@@ -149,6 +176,12 @@ class DistTransport:
 
     def exchange(self, sends, recvs):
         """sends/recvs: lists of (peer, tensor); one grouped p2p batch."""
+        self.exchange_async(sends, recvs).wait()
+
+    def exchange_async(self, sends, recvs):
+        """Start the grouped p2p batch and return a handle; the transfers run
+        on the communicator's stream (NCCL over NVLink) while the caller keeps
+        issuing work that does not touch the receive buffers, then wait()."""
         if self.stage:
             sends = [(peer, t.detach().to("cpu")) for peer, t in sends]
             staged = [(peer, torch.empty(t.shape, dtype=t.dtype), t) for peer, t in recvs]
@@ -160,11 +193,8 @@ class DistTransport:
         ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group)
                 for peer, t in recvs_h]
         if not ops:
-            return
-        for req in self.dist.batch_isend_irecv(ops):
-            req.wait()
-        for _, h, t in staged:
-            t.copy_(h)
+            return _Done()
+        return _Pending(self.dist.batch_isend_irecv(ops), staged)
 
     def sum_ordered(self, value):
         """Rank-ascending sum of per-rank partials, identical on every rank."""

@@ -118,3 +118,57 @@ def test_cycle_variants_match_oracle_engine(kind, nested):
     np.testing.assert_allclose([run.initial_residual] + run.residual_norms,
                                [ro.initial_residual] + ro.residual_norms, rtol=1e-10)
     np.testing.assert_allclose(sol.numpy(), so, rtol=0, atol=1e-12 * np.abs(so).max())
+
+
+# --- worker-count invariance on a deep hierarchy (reference acceptance test 7,
+# test_acceptance.py:229-267: 5 levels, p = 1, 2, 4) -------------------------------
+
+def _spec5():
+    return configs.config2(N=16, n_steps=320, levels=5, grids=2, strategy="delayed")
+
+
+def _solve5(transport):
+    from cpu_double import CpuDoubleProblem
+    from paper_1912_03106_b200 import (CycleSpec, MgritSolver, StoppingCriterion,
+                                       TimeHierarchy, build_uniform_grid)
+    spec = _spec5()
+    grid = build_uniform_grid(0.0, spec["tf"] * 320 / 2 ** 14, spec["n_steps"])
+    # ragged on purpose: 320 = 2 * 2 * 2 * 2 * 20 leaves F-tails and ranks
+    # without intervals on the coarse levels
+    solver = MgritSolver(CpuDoubleProblem(spec), TimeHierarchy.build(grid, [3, 2, 2, 2]),
+                         CycleSpec(kind="V", gamma=1, max_iters=8, spatial_strategy="delayed"),
+                         StoppingCriterion(tolerance=1e-9), transport)
+    return solver.solve(gather_solution=True)
+
+
+def _worker5(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+    from paper_1912_03106_b200 import DistTransport
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        run, sol = _solve5(DistTransport())
+        np.savez(os.path.join(out_dir, f"w{world}_rank{rank}.npz"),
+                 hist=np.array([run.initial_residual] + run.residual_norms),
+                 iters=run.iterations,
+                 sol=sol.numpy() if sol is not None else np.zeros(0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_five_level_solution_independent_of_worker_count(tmp_path, world):
+    from paper_1912_03106_b200 import NullTransport
+    run1, sol1 = _solve5(NullTransport())
+    h1 = np.array([run1.initial_residual] + run1.residual_norms)
+    mp.spawn(_worker5, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    scale = np.abs(sol1.numpy()).max()
+    for r in range(world):
+        z = np.load(tmp_path / f"w{world}_rank{r}.npz")
+        assert int(z["iters"]) == run1.iterations
+        np.testing.assert_allclose(z["hist"], h1, rtol=1e-10)
+    z0 = np.load(tmp_path / f"w{world}_rank0.npz")
+    assert np.abs(z0["sol"] - sol1.numpy()).max() <= 1e-10 * scale
