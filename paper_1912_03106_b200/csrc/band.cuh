@@ -58,17 +58,21 @@ struct BandFactorArgs {
 };
 
 __global__ void __launch_bounds__(256)
-k_band_build(BandFactorArgs a, const double* __restrict__ cvals, double* const* LBs) {
+k_band_build(BandFactorArgs a, const double* __restrict__ cvals, double* const* LBs,
+             const double* const* kper) {
     const int f = blockIdx.y;
     const double c = cvals[f];
     double* LB = LBs[f];
+    // per-factor stiffness values on the same CSR pattern (frozen Newton
+    // Jacobians); NULL: the level's own stiffness for every factor
+    const double* kv = kper ? kper[f] : a.k_val;
     const int stride = a.w + 1;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
         double* row = LB + (size_t)i * stride;
         for (int d = 0; d <= a.w; ++d) row[d] = 0.0;
         for (int e = a.row_ptr[i]; e < a.row_ptr[i + 1]; ++e) {
             const int j = a.col_idx[e];
-            if (j <= i) row[i - j] += fma(c, a.m_val[e], a.k_val[e]);
+            if (j <= i) row[i - j] += fma(c, a.m_val[e], kv[e]);
         }
     }
 }

@@ -171,6 +171,37 @@ __global__ void k_nk_japply(NkLevel L, const int* __restrict__ act,
     }
 }
 
+// Jacobian of column b's state as CSR values on the level's pattern (thread
+// per row): kj = K_lin + sum over the row's iron elements of
+// area [nu G^T G + 2 nu' (G^T g)(G^T g)^T] -- the matrix k_nk_japply applies
+// matrix-free, minus the c M term (k_band_build adds it).  Its banded
+// Cholesky factor is a frozen-Jacobian preconditioner for later Newton
+// systems with a similar saturation pattern.
+__global__ void k_nk_jac_assemble(NkLevel L, int b, const double* __restrict__ E,
+                                  double* __restrict__ kj) {
+    const double* Eb = E + (size_t)b * L.n_elem * 4;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += gridDim.x * blockDim.x) {
+        const int r0 = L.row_ptr[i], r1 = L.row_ptr[i + 1];
+        for (int k = r0; k < r1; ++k) kj[k] = L.k_val[k];
+        for (int k = L.ne_ptr[i]; k < L.ne_ptr[i + 1]; ++k) {
+            const int ea = L.ne[k], e = ea >> 2, a = ea & 3;
+            const double* gq = L.egeo + (size_t)e * 7;
+            const double* q = Eb + (size_t)e * 4;
+            const double ga = fma(q[2], gq[a], q[3] * gq[3 + a]);
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb) {
+                const int dof = L.edof[e * 3 + bb];
+                if (dof < 0) continue;
+                const double gg = fma(gq[a], gq[bb], gq[3 + a] * gq[3 + bb]);
+                const double gb = fma(q[2], gq[bb], q[3] * gq[3 + bb]);
+                const double v = gq[6] * fma(q[0], gg, q[1] * ga * gb);
+                for (int m = r0; m < r1; ++m)
+                    if (L.col_idx[m] == dof) { kj[m] += v; break; }
+            }
+        }
+    }
+}
+
 // r = -F, d = 0                                   grid (row chunks, active)
 __global__ void k_nk_start(int n, const int* __restrict__ act, int* __restrict__ flag,
                            const double* __restrict__ F,

@@ -96,6 +96,12 @@ struct Level {
     int nk_B = 0;
     std::vector<int> tmp_sub;      // column subset tmp_group was built for
     int tmp_BC = 0;
+    // frozen-Jacobian preconditioners of the Newton systems: per (source sign
+    // class, 1/dt bin) the banded factor of J at a converged state
+    struct JacPre { int fid = -1; int calls = 0; int builds = 0; };
+    std::unordered_map<uint64_t, JacPre> jac_pre;
+    double* kj = nullptr;          // [kj_cap][nnz] assembled Jacobian values
+    int kj_cap = 0;
     int* d_status = nullptr;
     // nonlinear iron elements
     int n_elem = 0;
@@ -341,6 +347,7 @@ static void free_level(Level& L) {
         if (p) cudaFree(p);
     if (L.nk_act) cudaFree(L.nk_act);
     if (L.nk_flag) cudaFree(L.nk_flag);
+    if (L.kj) cudaFree(L.kj);
 }
 
 extern "C" void pg_destroy(pg_ctx* ctx) {
@@ -946,7 +953,7 @@ static size_t band_solve_smem(const Level& L, int BC) {
 }
 
 static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
-                        cudaStream_t st) {
+                        cudaStream_t st, const std::vector<const double*>* kper = nullptr) {
     const int nf = (int)cs.size();
     if (!nf) return PG_OK;
     const int first = (int)L.FL.size();
@@ -1020,10 +1027,20 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     CU(cudaMalloc(&d_c, nf * sizeof(double)));
     CU(cudaMemcpyAsync(d_lb, lbs.data(), nf * sizeof(double*), cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_c, cs.data(), nf * sizeof(double), cudaMemcpyHostToDevice, st));
+    const double** d_kper = nullptr;
+    struct KperGuard {
+        const double**& p;
+        ~KperGuard() { if (p) cudaFree((void*)p); }
+    } kguard{d_kper};
+    if (kper) {
+        CU(cudaMalloc((void**)&d_kper, nf * sizeof(double*)));
+        CU(cudaMemcpyAsync((void*)d_kper, kper->data(), nf * sizeof(double*), cudaMemcpyHostToDevice,
+                           st));
+    }
     BandFactorArgs a{L.n, L.bw, L.bwin, L.LDA, L.nblk, L.row_ptr, L.col_idx, L.m_val,
                      L.n_elem > 0 ? L.k_pre : L.k_val};
     dim3 gb(std::min(1024, (L.n + 255) / 256), nf);
-    k_band_build<<<gb, 256, 0, st>>>(a, d_c, d_lb);
+    k_band_build<<<gb, 256, 0, st>>>(a, d_c, d_lb, d_kper);
     LAUNCHED();
     const size_t sm = (size_t)(2 * BD_NB * (BD_NB + 1) + L.bw * (BD_NB + 1) +
                                BD_NB * bd_cw(L.bwin)) * sizeof(double);
@@ -1072,6 +1089,7 @@ static int launch_rb(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, cudaStream
         return launch_rb_t<BC, CW, NCHK, FWD, 2, 1, 4>(ctx, sa, grid, st);
     } else {
         if (alt == 1) return launch_rb_t<BC, CW, NCHK, FWD, 4, 2, 1>(ctx, sa, grid, st);
+        if (alt == 2) return launch_rb_t<BC, CW, NCHK, FWD, 2, 2, 4>(ctx, sa, grid, st);
         return launch_rb_t<BC, CW, NCHK, FWD, 2, 2, 2>(ctx, sa, grid, st);
     }
 }
@@ -1336,7 +1354,10 @@ static int factor_ids(pg_ctx* ctx, Level& L, const double* c, int n, int* fid,
 static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* inv_dt,
                     const double* inv_dt_host, const double* src, double* u_out,
                     const double* g, const int* g_idx, cudaStream_t st,
-                    const double* copy_src = nullptr, const int* sub = nullptr) {
+                    const double* copy_src = nullptr, const int* sub = nullptr,
+                    const int* fid_all = nullptr) {
+    // fid_all (preconditioner mode): factor of every full-batch column, chosen
+    // by the caller (frozen-Jacobian preconditioners) instead of by 1/dt
     std::vector<double> c(B);
     if (sub) {
         // preconditioner mode: inv_dt_host is the full-batch host array
@@ -1367,7 +1388,11 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     std::vector<int> fid;
     if (!grp) {
         fid.resize(B);
-        if ((rc = factor_ids(ctx, L, c.data(), B, fid.data(), st))) return rc;
+        if (sub && fid_all) {
+            for (int j = 0; j < B; ++j) fid[j] = fid_all[sub[j]];
+        } else if ((rc = factor_ids(ctx, L, c.data(), B, fid.data(), st))) {
+            return rc;
+        }
         // group columns by factor -> perm, chunks of BC
         std::vector<int> perm(B);
         for (int b = 0; b < B; ++b) perm[b] = b;
@@ -1747,6 +1772,15 @@ extern "C" int pg_fas_rhs(pg_ctx* ctx, int coarse, int coarsen, int B, const dou
     const int sf = coarsen ? ctx->levels[coarse - 1].side : sc;
     if (coarsen && sf != 2 * sc + 1) return set_err(ctx, PG_EINVAL, "grids not nested");
     CU(cudaSetDevice(ctx->device));
+    if (!coarsen) {
+        // same grid: a flat pass over n B entries (any level, structured or not)
+        const size_t total = (size_t)ctx->levels[coarse].n * B;
+        if (total > 0x7fffffffull) return set_err(ctx, PG_EINVAL, "batch too large");
+        k_fas_rhs<<<grid_for(ctx, total), 256, 0, (cudaStream_t)stream>>>(
+            1, 1, 0, (int)total, kept, cprop, res, rhs, mode);
+        LAUNCHED();
+        return PG_OK;
+    }
     k_fas_rhs<<<grid_for(ctx, (size_t)sc * sc * B), 256, 0, (cudaStream_t)stream>>>(
         sf, sc, coarsen, B, kept, cprop, res, rhs, mode);
     LAUNCHED();

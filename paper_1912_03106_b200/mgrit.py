@@ -18,6 +18,7 @@ redistribution and the coarsest gather/scatter are grouped p2p
 """
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -185,6 +186,9 @@ class _Level:
             self.rhs = torch.zeros(self.n_owned, self.n, **f64)
         self.use_rhs = False
         self.seconds = 0.0
+        self.chain_vals = None          # coarsest chain values (rank 0)
+        self.full_rhs = None            # gathered coarsest rhs (rank 0, multi-rank)
+        self.chain_graphs = {}          # captured coarsest chains
         # per-point tables (device): 1/dt and source values at t_next
         t = self.t
         inv = np.zeros(self.n_points)
@@ -253,10 +257,16 @@ class MgritSolver:
                 if vals:
                     problem.prefactor(s_lvl, np.unique(np.concatenate(vals)))
         self._plans = {}
+        # CUDA-graph replay of the coarsest chain: problems opt in
+        # (graph_safe: Phi launches with no host read); PINTGPU_GRAPHS=0 disables
+        self._graphs = (bool(getattr(problem, "graph_safe", False))
+                        and os.environ.get("PINTGPU_GRAPHS", "1") != "0")
         self._smooth = False
         self._probe_prop = None      # probe result reusable by the next level-0 FC sweep
         import inspect
         self._takes_host_dt = "inv_dt_host" in inspect.signature(problem.phi_batch).parameters
+        # without the host copy of 1/dt Phi reads it back (a sync): not capturable
+        self._graphs = self._graphs and self._takes_host_dt
         self.phi_columns = 0
         self.phi_calls = 0
         self.setup_seconds = time.perf_counter() - t_setup
@@ -450,7 +460,9 @@ class MgritSolver:
             full = None
             if lvl.use_rhs:
                 if T.rank == 0:
-                    full = torch.zeros(n_pts, lvl.n, dtype=torch.float64, device=dev)
+                    if lvl.full_rhs is None:
+                        lvl.full_rhs = torch.zeros(n_pts, lvl.n, dtype=torch.float64, device=dev)
+                    full = lvl.full_rhs
                     recvs = []
                     for w in active:
                         lo, hi = lvl.decomp.owned_range(w)
@@ -464,11 +476,7 @@ class MgritSolver:
             g, g_idx = (full, lvl.pt_idx) if full is not None else (None, None)
         vals = None
         if T.rank == 0:
-            vals = torch.empty(n_pts, lvl.n, dtype=torch.float64, device=dev)
-            vals[0].copy_(lvl.anchor)
-            for i in range(1, n_pts):
-                self._phi_pts(lvl, vals[i - 1:i], i, i + 1, vals[i:i + 1],
-                              g=g, g_idx=None if g is None else g_idx[i:i + 1])
+            vals = self._coarsest_chain(lvl, g, g_idx)
         # scatter
         if single:
             mine = vals[lvl.own_lo:lvl.own_hi]
@@ -498,6 +506,56 @@ class MgritSolver:
                 torch.index_select(lvl.u_keep, 0, rows, out=lvl.c_store)
             else:
                 lvl.c_store.add_(lvl.u_keep.index_select(0, rows))
+
+    def _coarsest_chain(self, lvl, g, g_idx):
+        """The serial chain v_i = Phi(v_{i-1}) (+ g_i) over the coarsest grid on
+        rank 0 (mgrit.py:468-480): one single-column Phi per point, all on the
+        device.  For problems whose Phi launches without host reads (linear,
+        banded Cholesky) the chain of a level is captured into a CUDA graph the
+        second time it runs -- same points, same factors, same buffers in every
+        cycle -- and replayed afterwards, so later cycles pay one graph launch
+        instead of ~10 kernel launches per point."""
+        n_pts = lvl.n_points
+        if lvl.chain_vals is None:
+            lvl.chain_vals = torch.empty(n_pts, lvl.n, dtype=torch.float64,
+                                         device=self.problem.device)
+        vals = lvl.chain_vals
+        vals[0].copy_(lvl.anchor)
+
+        def run():
+            for i in range(1, n_pts):
+                self._phi_pts(lvl, vals[i - 1:i], i, i + 1, vals[i:i + 1],
+                              g=g, g_idx=None if g is None else g_idx[i:i + 1])
+
+        key = (self._smooth, None if g is None else g.data_ptr())
+        entry = lvl.chain_graphs.get(key)
+        if not self._graphs or n_pts < 3:
+            run()
+        elif entry is None:
+            run()                                   # warms factors, spikes, groupings
+            lvl.chain_graphs[key] = "warm"
+        elif entry == "warm":
+            graph = torch.cuda.CUDAGraph()
+            calls, cols = self.phi_calls, self.phi_columns
+            try:
+                with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                    run()
+                lvl.chain_graphs[key] = (graph, self.phi_calls - calls,
+                                         self.phi_columns - cols)
+                graph.replay()
+            except Exception:                       # not capturable here: stay eager
+                self._graphs = False
+                lvl.chain_graphs.clear()
+                self.phi_calls, self.phi_columns = calls, cols
+                torch.cuda.synchronize(self.problem.device)
+                vals[0].copy_(lvl.anchor)
+                run()
+        else:
+            graph, calls, cols = entry
+            graph.replay()
+            self.phi_calls += calls
+            self.phi_columns += cols
+        return vals
 
     def _ascend(self, coarse, fine, inject=False, solved=False):
         """mgrit.py:497-571: coarse walk (unless solved) turning u_keep into

@@ -96,6 +96,10 @@ class GpuFemProblem:
                    "pg_set_options")
         self._weights = [torch.as_tensor(g.weights, device=self.device) for g in self.grids]
         self.nonlinear = bool(spec.get("nonlinear"))
+        # Phi of a linear level with the banded factors launches kernels only
+        # (no host read, no allocation once warm): safe to capture in a CUDA graph
+        self.graph_safe = (not self.nonlinear and kind == "cholesky"
+                           and type(self) is GpuFemProblem)
 
     def _add_level(self, g):
         arrays = dict(row_ptr=np.ascontiguousarray(g.row_ptr, np.int32),

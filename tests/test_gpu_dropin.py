@@ -50,6 +50,9 @@ def test_reference_1d_operator_through_phi_batch(cuda, inner):
     assert np.array_equal(prob.grids[0].shapes[0], fx["shape"])
     assert np.allclose(prob.loss_weights(0).cpu().numpy(), fx["weights"], rtol=0, atol=0)
     B = fx["U"].shape[0]
+    # the banded direct solve is the reference's algorithm (1e-12, its own
+    # test's bar); Jacobi-PCG at rtol 1e-13 is an iterative stand-in
+    rtol = 1e-12 if inner == "cholesky" else 1e-9
     U = torch.as_tensor(fx["U"], device=cuda)
     inv = 1.0 / (fx["t_next"] - fx["t_prev"])
     for smooth, key, skey in ((False, "out", "src"), (True, "out_smooth", "src_smooth")):
@@ -59,17 +62,17 @@ def test_reference_1d_operator_through_phi_batch(cuda, inner):
         prob.phi_batch(0, U, torch.as_tensor(inv, device=cuda), torch.as_tensor(src, device=cuda),
                        out, inv_dt_host=np.ascontiguousarray(inv))
         got = out.cpu().numpy()
-        assert np.allclose(got, fx[key], rtol=1e-12, atol=1e-14)
+        assert np.allclose(got, fx[key], rtol=rtol, atol=1e-14)
         for b in range(B):
             dense = _dense_step(n, nu, sigma, 1.0 / inv[b], fx["U"][b], src[b, 0] * fx["shape"])
-            assert np.allclose(got[b], dense, rtol=1e-12, atol=1e-14)
+            assert np.allclose(got[b], dense, rtol=rtol, atol=1e-14)
     # the B = 1 contract view: fresh state, inputs untouched, deterministic
     from paper_1912_03106_b200 import BlockState
     u0 = BlockState(U[0].clone())
     a, diag = prob.step(u0, float(fx["t_prev"][0]), float(fx["t_next"][0]))
     b, _ = prob.step(u0, float(fx["t_prev"][0]), float(fx["t_next"][0]))
     assert torch.equal(a.field, b.field) and torch.equal(u0.field, U[0]) and diag.converged
-    assert np.allclose(a.field.cpu().numpy(), fx["out"][0], rtol=1e-12, atol=1e-14)
+    assert np.allclose(a.field.cpu().numpy(), fx["out"][0], rtol=rtol, atol=1e-14)
     prob.close()
 
 

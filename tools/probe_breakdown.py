@@ -46,6 +46,8 @@ def timed(level, U, *a, **k):
     return r
 
 
+import inspect
+timed.__signature__ = inspect.signature(orig)
 prob.phi_batch = timed
 t0 = time.perf_counter()
 run, _ = make().solve(gather_solution=False)
