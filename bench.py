@@ -30,6 +30,7 @@ roofline: per-kernel table from a separate, untimed profiling solve (CUDA
 config2: the config-2 leg (127^2, 2^14 steps, 3 levels): time-to-solution and
          its residual history checked against the reference engine's own
          full-size run (tests/golden/mgrit_cfg2_full.npz).
+config3: the nonlinear config-3 leg at its stated size: one solve.
 phi_microbench: BASELINE config 5 (256^2 Jacobi-PCG Phi, B = 64 .. 4096).
 sequential_gpu: GPU sequential stepping on a window of the headline,
          extrapolated to the whole horizon (labelled).
@@ -412,6 +413,44 @@ def config2_leg(local, transport, reps=3):
     return res
 
 
+def config3_leg(local, transport):
+    """Config 3 at its stated size (nonlinear Brauer iron, 127^2, 2^14 steps,
+    3 levels): one solve -- damped Newton per column, CG on the Newton systems
+    preconditioned by frozen-Jacobian banded factors."""
+    import torch
+    from paper_1912_03106_b200 import (CycleSpec, GpuFemProblem, MgritSolver, StoppingCriterion,
+                                       TimeHierarchy, build_uniform_grid, configs)
+    spec = configs.config3(grids=2, strategy="delayed")
+    mg = spec["mgrit"]
+    prob = GpuFemProblem(spec, device=local)
+    grid = build_uniform_grid(0.0, spec["tf"], spec["n_steps"])
+    solver = MgritSolver(prob, TimeHierarchy.build(grid, mg["factors"]),
+                         CycleSpec(kind=mg["kind"], gamma=mg["gamma"], max_iters=mg["max_iters"],
+                                   spatial_strategy=mg["spatial_strategy"]),
+                         StoppingCriterion(tolerance=mg["tolerance"]), transport)
+    dev = prob.device
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    run, _ = solver.solve(gather_solution=False)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = e0.elapsed_time(e1) / 1e3
+    st = prob.total_stats()
+    res = {"workload": "BASELINE config 3: nonlinear (Brauer iron annulus), 128x128 grid, 2^14 "
+                       "steps, 3 levels, delayed spatial coarsening, Newton tol 1e-8",
+           "time_to_solution_s": t, "value": spec["n_steps"] * prob.spatial.size(0) / t,
+           "unit": "fine time-step*DOF/s", "iterations": run.iterations,
+           "converged": run.converged, "failure": run.failure,
+           "residual_history": _history(run),
+           "newton_iterations": st["newton_iters"], "batched_cg_iterations": st["column_iters"],
+           "note": "first solve of a fresh problem (includes building the frozen-Jacobian "
+                   "factors); parity pinned at 63^2 by tests/golden/mgrit_cfg3_n64.npz"}
+    prob.close()
+    return res
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -565,6 +604,7 @@ def run_b200(args):
     del host
 
     cfg2 = config2_leg(local, transport) if not args.no_cfg2 else None
+    cfg3 = config3_leg(local, transport) if not args.no_cfg3 else None
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -624,6 +664,7 @@ def run_b200(args):
         "roofline": roofline,
         "sequential_gpu": seq,
         "config2": cfg2,
+        "config3": cfg3,
         "phi_microbench": phi_bench,
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
@@ -664,6 +705,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-phi", action="store_true", help="skip the config-5 batched-Phi leg")
     ap.add_argument("--no-cfg2", action="store_true", help="skip the config-2 leg")
+    ap.add_argument("--no-cfg3", action="store_true", help="skip the config-3 (nonlinear) leg")
     ap.add_argument("--e2e-reps", type=int, default=1,
                     help="end-to-end repetitions (median reported)")
     ap.add_argument("--no-seq", action="store_true", help="skip the GPU sequential-stepping leg")

@@ -77,11 +77,25 @@ k_band_build(BandFactorArgs a, const double* __restrict__ cvals, double* const* 
     }
 }
 
-// smem: D[32][33], Dinv[32][33], P[w][33], Lw[32][CW] (one window chunk)
+// smem: D[32][36], Dinv[32][36], P[wp][36] (wp = w rounded up to 32, rows past
+// the panel zero), Lw[32][CW + 4] (one window chunk).  Row strides of 4 mod 16
+// doubles keep the DMMA fragment loads of a half-warp on distinct bank pairs.
 // Per block row k it emits FL[k] = [D_k^-1 | D_k^-1 L_win] and
 // FU[k] = [D_k^-T | D_k^-T U_win] (32 x LDA, LDA = 32 + W + 4): the solve
 // step is y_k = D_k^-1 b_k - (D_k^-1 L_win) y_win, whose first term does not
 // depend on the chain.
+// The two GEMM-shaped parts of a block step run on the fp64 tensor cores
+// (mma.sync m8n8k4, SASS DMMA): the solve operands (32 x 32 times 32 x W,
+// twice) and the trailing update A -= P P^T of the w x w window (8.4 MFLOP per
+// step at w = 512: as scalar FMAs with two shared-memory loads each it was
+// 85 % of the factorisation time, round 2).  Warp w of 8 takes every 8th
+// 32 x 32 super-tile of the lower triangle: 8 fragment loads per 16 DMMAs.
+#define BD_FS 36
+__host__ __device__ constexpr int bd_factor_wp(int w) { return (w + 31) / 32 * 32; }
+__host__ __device__ constexpr size_t bd_factor_smem(int w, int cw) {
+    return (size_t)(2 * BD_NB * BD_FS + bd_factor_wp(w) * BD_FS + BD_NB * (cw + 4)) * sizeof(double);
+}
+
 __global__ void __launch_bounds__(256)
 k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* const* FUs,
               int* status) {
@@ -90,13 +104,15 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
     double* LB = LBs[f];
     double* FL = FLs[f];
     double* FU = FUs[f];
-    const int NB = BD_NB, S = NB + 1;
+    constexpr int NB = BD_NB, S = BD_FS;
+    const int wp = bd_factor_wp(a.w);
     double* D = sm;
     double* Di = D + NB * S;
     double* P = Di + NB * S;
-    double* Lw = P + (size_t)a.w * S;
+    double* Lw = P + (size_t)wp * S;
     const int stride = a.w + 1;
     const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q4 = lane & 3;
     auto lb = [&](int i, int j) -> double& { return LB[(size_t)i * stride + (i - j)]; };
     // unconditional read of band entry (i, j): the address is clamped into the
     // band so the load never depends on a branch (loads of a row issue together)
@@ -106,6 +122,8 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
         const double v = LB[(size_t)ii * stride + d];
         return ok ? v : 0.0;
     };
+    for (int t = tid; t < wp * S; t += blockDim.x) P[t] = 0.0;
+    int m_prev = wp;
 
     for (int k = 0; k < a.nblk; ++k) {
         const int k0 = k * NB;
@@ -166,6 +184,9 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
 #pragma unroll
             for (int j = 0; j < NB; ++j) P[r * S + j] = x[j];
         }
+        // rows past the panel stay zero (the panel shrinks at the end of the band)
+        for (int t = m * S + tid; t < m_prev * S; t += blockDim.x) P[t] = 0.0;
+        m_prev = m;
         __syncthreads();
         // write L back into the band (diagonal block + panel)
         for (int t = tid; t < NB * NB; t += blockDim.x) {
@@ -179,7 +200,7 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
         }
         // 5. solve operands of block k, piece by piece (layout: bd_block_doubles)
         {
-            const int CW = bd_cw(a.W), nchk = a.W / CW;
+            const int CW = bd_cw(a.W), nchk = a.W / CW, LW = CW + 4;
             double* fl = FL + (size_t)k * bd_block_doubles(a.W);
             double* fu = FU + (size_t)k * bd_block_doubles(a.W);
             for (int t = tid; t < NB * BD_PD; t += blockDim.x) {
@@ -190,40 +211,92 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
             for (int c = 0; c < nchk; ++c) {
                 // Lw[i][q] = L[k0+i][k0-W+c CW+q] (final: earlier panels)
                 for (int t = tid; t < NB * CW; t += blockDim.x) {
-                    const int i = t / CW, q = c * CW + t % CW;
+                    const int i = t / CW, ql = t % CW, q = c * CW + ql;
                     const int gr = k0 + i, gc = k0 - a.W + q;
-                    Lw[t] = lbv(gr, max(gc, 0), i < kb && gc >= 0 && gr - gc <= a.w);
+                    Lw[i * LW + ql] = lbv(gr, max(gc, 0), i < kb && gc >= 0 && gr - gc <= a.w);
                 }
                 __syncthreads();
-                double* flc = fl + NB * BD_PD + (size_t)c * NB * (CW + 4);
-                double* fuc = fu + NB * BD_PD + (size_t)c * NB * (CW + 4);
-                for (int t = tid; t < NB * (CW + 4); t += blockDim.x) {
-                    const int i = t / (CW + 4), ql = t % (CW + 4), q = c * CW + ql;
-                    double vl = 0.0, vu = 0.0;
-                    if (ql < CW) {
-                        // (D^-1 L_win)[i][q] = sum_p Di[i][p] Lw[p][q]
-#pragma unroll 8
-                        for (int p = 0; p <= i; ++p) vl = fma(Di[i * S + p], Lw[p * CW + ql], vl);
-                        // (D^-T U_win)[i][q] = sum_p Di[p][i] P[q][p]
-                        if (q < m) {
-#pragma unroll 8
-                            for (int p = i; p < NB; ++p) vu = fma(Di[p * S + i], P[q * S + p], vu);
+                double* flc = fl + NB * BD_PD + (size_t)c * NB * LW;
+                double* fuc = fu + NB * BD_PD + (size_t)c * NB * LW;
+                // (D^-1 L_win)[i][q] = sum_p Di[i][p] Lw[p][q]     (Di lower, zeros stored)
+                // (D^-T U_win)[i][q] = sum_p Di[p][i] P[q][p]      (P rows >= m are zero)
+                // 32 x CW each: 8-column tiles dealt round-robin to the warps
+                for (int nt = warp; nt < CW / 8; nt += 8) {
+                    double cl[4][2], cu[4][2];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) cl[mi][0] = cl[mi][1] = cu[mi][0] = cu[mi][1] = 0.0;
+                    const int qb = c * CW + 8 * nt;              // first window column of the tile
+#pragma unroll
+                    for (int u = 0; u < NB / 4; ++u) {
+                        const int kk = 4 * u + q4;
+                        const double bl = Lw[kk * LW + 8 * nt + g];
+                        const double bu = qb + g < wp ? P[(qb + g) * S + kk] : 0.0;
+#pragma unroll
+                        for (int mi = 0; mi < 4; ++mi) {
+                            dmma_8x8x4(cl[mi][0], cl[mi][1], Di[(8 * mi + g) * S + kk], bl);
+                            dmma_8x8x4(cu[mi][0], cu[mi][1], Di[kk * S + 8 * mi + g], bu);
                         }
                     }
-                    flc[t] = vl;
-                    fuc[t] = vu;
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int o = (8 * mi + g) * LW + 8 * nt + 2 * q4 + h;
+                            flc[o] = cl[mi][h];
+                            fuc[o] = cu[mi][h];
+                        }
+                }
+                // the 4 pad columns of every row
+                for (int t = tid; t < NB * 4; t += blockDim.x) {
+                    const int o = (t / 4) * LW + CW + t % 4;
+                    flc[o] = 0.0;
+                    fuc[o] = 0.0;
                 }
                 __syncthreads();
             }
         }
-        // 6. trailing update of the band: A[r][s] -= P[r] . P[s], s <= r
-        for (int t = tid; t < m * m; t += blockDim.x) {
-            const int r = t / m, s = t % m;
-            if (s > r || r - s > a.w) continue;
-            double acc = 0.0;
-#pragma unroll 8
-            for (int j = 0; j < NB; ++j) acc = fma(P[r * S + j], P[s * S + j], acc);
-            lb(r0 + r, r0 + s) -= acc;
+        // 6. trailing update of the band: A[r][s] -= P[r] . P[s], s <= r, by
+        // 32 x 32 super-tiles of the lower triangle
+        {
+            const int nR = (m + 31) / 32, nST = nR * (nR + 1) / 2;
+            for (int idx = warp; idx < nST; idx += 8) {
+                int R = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+                while (R * (R + 1) / 2 > idx) --R;
+                while ((R + 1) * (R + 2) / 2 <= idx) ++R;
+                const int Sx = idx - R * (R + 1) / 2;
+                double acc[4][4][2];
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+                const double* pa = P + (32 * R + g) * S + q4;
+                const double* pb = P + (32 * Sx + g) * S + q4;
+#pragma unroll
+                for (int u = 0; u < NB / 4; ++u) {
+                    double av[4], bv[4];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) av[mi] = pa[8 * mi * S + 4 * u];
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni) bv[ni] = pb[8 * ni * S + 4 * u];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                        for (int ni = 0; ni < 4; ++ni)
+                            dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+                }
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi) {
+                    const int r = 32 * R + 8 * mi + g;
+                    if (r >= m) continue;
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int sc = 32 * Sx + 8 * ni + 2 * q4 + h;
+                            if (sc <= r) lb(r0 + r, r0 + sc) -= acc[mi][ni][h];
+                        }
+                }
+            }
         }
         __syncthreads();
     }

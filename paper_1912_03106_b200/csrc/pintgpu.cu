@@ -1042,8 +1042,7 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     dim3 gb(std::min(1024, (L.n + 255) / 256), nf);
     k_band_build<<<gb, 256, 0, st>>>(a, d_c, d_lb, d_kper);
     LAUNCHED();
-    const size_t sm = (size_t)(2 * BD_NB * (BD_NB + 1) + L.bw * (BD_NB + 1) +
-                               BD_NB * bd_cw(L.bwin)) * sizeof(double);
+    const size_t sm = bd_factor_smem(L.bw, bd_cw(L.bwin));
     CU(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_band_factor<<<nf, 256, sm, st>>>(a, d_lb, L.d_FL + first, L.d_FU + first, L.d_status);
     LAUNCHED();

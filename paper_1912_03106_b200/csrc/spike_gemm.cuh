@@ -5,8 +5,8 @@
 // fp64 tensor-core GEMM (mma.sync m8n8k4.f64, SASS DMMA).  One CTA owns a
 // 128-row x 64-column tile of one chunk and one factor; 8 warps as 4 (rows) x
 // 2 (columns), 4 x 4 DMMA tiles per warp, so a k-step of 4 costs 8 fragment
-// loads for 16 DMMAs.  Operands stream through a 2-stage cp.async ring in
-// K-steps of 16:
+// loads for 16 DMMAs.  Operands stream through a 4-stage cp.async ring in
+// K-steps of 16 (three stages in flight, one barrier per K-step):
 //     A = G[k][row]   (row contiguous in HBM: [W][ldy])       smem As[k][128 + 4]
 //     B = T[col][k]   (k contiguous: [P][ldt][W])             smem Bs[col][16 + 4]
 // Row strides of 4 mod 16 doubles make the 8 x 4 (A) and 4 x 8 (B) fragment
@@ -21,7 +21,8 @@
 #define SG_KS 16
 #define SG_AP (SG_TM + 4)
 #define SG_BP (SG_KS + 4)
-#define SG_SMEM ((size_t)2 * (SG_KS * SG_AP + SG_TN * SG_BP) * sizeof(double))
+#define SG_NST 4
+#define SG_SMEM ((size_t)SG_NST * (SG_KS * SG_AP + SG_TN * SG_BP) * sizeof(double))
 
 __device__ __forceinline__ void sg_cp16(void* dst, const void* src, int src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
@@ -35,8 +36,8 @@ template <bool FWD>
 __global__ void __launch_bounds__(256, 2)
 k_spike_gemm(SpikeArgs a, const int4* __restrict__ tiles) {
     extern __shared__ __align__(16) double sg[];
-    double* As = sg;                                   // [2][KS][AP]
-    double* Bs = sg + 2 * SG_KS * SG_AP;               // [2][TN][BP]
+    double* As = sg;                                   // [NST][KS][AP]
+    double* Bs = sg + SG_NST * SG_KS * SG_AP;          // [NST][TN][BP]
     const int4 tl = tiles[blockIdx.z];
     const double* G = a.G[tl.x];
     const int c0 = tl.y, nc = tl.z;
@@ -80,17 +81,18 @@ k_spike_gemm(SpikeArgs a, const int4* __restrict__ tiles) {
         for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
     const int nk = a.W / SG_KS;
-    stage_load(0, 0);
+#pragma unroll
+    for (int i = 0; i < SG_NST - 1; ++i) {
+        if (i < nk) stage_load(i, i * SG_KS);
+        else cp_async_commit();
+    }
     for (int ks = 0; ks < nk; ++ks) {
-        if (ks + 1 < nk) {
-            stage_load((ks + 1) & 1, (ks + 1) * SG_KS);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const double* as = As + (ks & 1) * SG_KS * SG_AP + wm * 32 + g;
-        const double* bs = Bs + (ks & 1) * SG_TN * SG_BP + (wn * 32 + g) * SG_BP;
+        cp_async_wait<SG_NST - 2>();      // stage ks has landed (this thread's copies)
+        __syncthreads();                  // ... everyone's; and stage ks - 1 is free again
+        if (ks + SG_NST - 1 < nk) stage_load((ks + SG_NST - 1) % SG_NST, (ks + SG_NST - 1) * SG_KS);
+        else cp_async_commit();
+        const double* as = As + (ks % SG_NST) * SG_KS * SG_AP + wm * 32 + g;
+        const double* bs = Bs + (ks % SG_NST) * SG_TN * SG_BP + (wn * 32 + g) * SG_BP;
 #pragma unroll
         for (int u = 0; u < SG_KS / 4; ++u) {
             double av[4], bv[4];
@@ -104,7 +106,6 @@ k_spike_gemm(SpikeArgs a, const int4* __restrict__ tiles) {
                 for (int ni = 0; ni < 4; ++ni)
                     dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
         }
-        __syncthreads();          // the stage is refilled by the next iteration's loads
     }
     // C fragment: row g, columns 2 q4, 2 q4 + 1 of each 8 x 8 tile
 #pragma unroll

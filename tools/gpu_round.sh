@@ -1,5 +1,7 @@
-# full GPU tests + smoke + default bench (dev)
+# full GPU tests + smoke + default bench + reference arm (dev)
 mkdir -p gpurun_out
-( time timeout 1500 python -m pytest tests -m gpu -x -q --durations=15 ) > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+( time timeout 1500 python -m pytest tests -m gpu -q --durations=8 ) > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 ( time timeout 1500 python bench.py ) > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 600 python tools/probe_breakdown.py cfg2 > gpurun_out/bd_cfg2.txt 2>&1
+PINTGPU_GRAPHS=0 timeout 600 python tools/probe_breakdown.py cfg2 > gpurun_out/bd_cfg2_nograph.txt 2>&1
