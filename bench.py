@@ -612,7 +612,13 @@ def run_b200(args):
     peak, peak_src = measured_peak()
     fpk, fpk_src = fp64_peak()
     kernels = summarize_kernels(prof, prof_elapsed, peak, fpk)
-    chains = [k for k in kernels if k["name"].startswith("band_chain")]
+    # dominant kernel: the 32-column-group chains (k_band_rb<32, ...>) of the
+    # GPU-filling level-0 batches; narrower batches (fewer ranks' worth of
+    # columns) fall back to all chain launches
+    chains = [k for k in kernels if k["name"].startswith("chain32")]
+    wide = bool(chains)
+    if not chains:
+        chains = [k for k in kernels if k["name"].startswith("band_chain")]
     roofline = None
     if chains:
         ms = sum(k["total_ms"] for k in chains)
@@ -621,15 +627,21 @@ def run_b200(args):
         nl = sum(k["launches"] for k in chains)
         tr = ncu_traffic()
         traffic = None
-        if tr and tr.get("workload") == "cfg4-headline":
+        if wide and tr and tr.get("workload") == "cfg4-headline":
             traffic = tr.get("dram_bytes_per_launch")
-        roofline = {"bound": "tensor", "kernel": "k_band_rb (band chains, fwd + bwd)",
+        roofline = {"bound": "tensor",
+                    "kernel": ("k_band_rb<32, ...> (band chains of the 4,096-column level-0 "
+                               "batches, fwd + bwd)" if wide else
+                               "band chains (k_band_rb / k_band_chain_ks, fwd + bwd)"),
                     "achieved": fl / (ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
                     "frac": fl / (ms * 1e-3) / 1e12 / fpk, "traffic": traffic,
+                    "traffic_source": (tr.get("source") if traffic else None),
+                    "alg_bytes_per_launch": by / nl,
                     "peak_source": fpk_src,
                     "share_of_step": (ms / 1e3) / prof_elapsed,
-                    "avg_launch_ms": ms / nl,
+                    "avg_launch_ms": ms / nl, "launches": nl,
                     "hbm_achieved_gbs": by / (ms * 1e-3) / 1e9, "hbm_peak_gbs": peak,
+                    "hbm_frac": by / (ms * 1e-3) / 1e9 / peak,
                     "hbm_peak_source": peak_src,
                     "alg_model": "flops 2 n w per direction and column (w = the band's lower "
                                  "bandwidth: the reference's dpbtrs); bytes = Y in/out + each "

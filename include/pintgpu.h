@@ -206,10 +206,12 @@ typedef struct pg_kernel_profile {
  * bracketed by CUDA events on the launching stream (and the call syncs).
  * pg_profile_read fills up to n of the PG_PROFILE_KINDS entries, in order:
  * k_sdir, k_supd (Jacobi-PCG), k_band_solve (= chains + SPIKE recombination),
- * band_chain_fwd, band_chain_bwd, band_rhs, spike_border, spike_fix,
- * band_scatter; alg_flops / alg_bytes are the algorithmic work (the
+ * band_chain_fwd, band_chain_bwd (column groups of 8 / 16), band_rhs,
+ * spike_border, spike_fix, band_scatter, chain32_fwd, chain32_bwd (the
+ * 32-column groups of GPU-filling batches, k_band_rb<32, ...>);
+ * alg_flops / alg_bytes are the algorithmic work (the
  * reference's dpbtrs: 2 n w flops per direction and column). */
-#define PG_PROFILE_KINDS 9
+#define PG_PROFILE_KINDS 11
 int  pg_profile(pg_ctx* ctx, int on);
 int  pg_profile_read(pg_ctx* ctx, pg_kernel_profile* out, int n, int reset);
 

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("PINTGPU_LIB") or os.path.join(
 
 PG_OK, PG_EINVAL, PG_ECUDA, PG_ENEWTON, PG_ENOCONV = 0, 1, 2, 3, 4
 PG_INNER_PCG, PG_INNER_CHOLESKY = 0, 1
-PG_PROFILE_KINDS = 9            # pintgpu.h
+PG_PROFILE_KINDS = 11           # pintgpu.h
 
 c_int, c_int32, c_int64, c_double = (ctypes.c_int, ctypes.c_int32,
                                      ctypes.c_int64, ctypes.c_double)

@@ -284,16 +284,25 @@ k_band_factor(BandFactorArgs a, double* const* LBs, double* const* FLs, double* 
                         for (int ni = 0; ni < 4; ++ni)
                             dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
                 }
+                // read-modify-write of the band, 8 loads in flight per lane
 #pragma unroll
                 for (int mi = 0; mi < 4; ++mi) {
                     const int r = 32 * R + 8 * mi + g;
-                    if (r >= m) continue;
+                    double* row = LB + (size_t)(r0 + r) * stride + r;    // entry (r, s) at row[-s]
+                    double old[4][2];
 #pragma unroll
                     for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int sc = 32 * Sx + 8 * ni + 2 * q4 + h;
-                            if (sc <= r) lb(r0 + r, r0 + sc) -= acc[mi][ni][h];
+                            old[ni][h] = (r < m && sc <= r) ? row[-sc] : 0.0;
+                        }
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int sc = 32 * Sx + 8 * ni + 2 * q4 + h;
+                            if (r < m && sc <= r) row[-sc] = old[ni][h] - acc[mi][ni][h];
                         }
                 }
             }

@@ -123,11 +123,11 @@ struct Level {
 // band-solve kinds (chains + SPIKE recombination) of a Phi call.
 enum {
     PG_PROF_SDIR = 0, PG_PROF_SUPD, PG_PROF_BAND, PG_PROF_FWD, PG_PROF_BWD, PG_PROF_RHS,
-    PG_PROF_BORDER, PG_PROF_FIX, PG_PROF_SCATTER, PG_PROF_N
+    PG_PROF_BORDER, PG_PROF_FIX, PG_PROF_SCATTER, PG_PROF_FWD_W, PG_PROF_BWD_W, PG_PROF_N
 };
 static const char* const PG_PROF_NAMES[PG_PROF_N] = {
     "k_sdir", "k_supd", "k_band_solve", "band_chain_fwd", "band_chain_bwd", "band_rhs",
-    "spike_border", "spike_fix", "band_scatter"};
+    "spike_border", "spike_fix", "band_scatter", "chain32_fwd", "chain32_bwd"};
 
 struct pg_ctx {
     int device = 0;
@@ -1513,7 +1513,10 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     for (int dir = 0; dir < 2 && !rc; ++dir) {
         const bool fwd = dir == 0;
         sa.F = fwd ? L.d_FL : L.d_FU;
-        const int pk = fwd ? PG_PROF_FWD : PG_PROF_BWD;
+        // 32-column groups (k_band_rb<32, ...>: the batches that fill the GPU)
+        // are profiled apart from the narrower, latency-bound chain launches
+        const int pk = BC == 32 ? (fwd ? PG_PROF_FWD_W : PG_PROF_BWD_W)
+                                : (fwd ? PG_PROF_FWD : PG_PROF_BWD);
         if ((rc = prof_mark(ctx, pk, st))) break;
         if ((rc = band_dir(ctx, L, BC, fwd, sa, dim3(nch, P), sm, st))) break;
         if ((rc = prof_mark(ctx, pk, st))) break;
@@ -1540,7 +1543,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         double fb = 0.0;
         for (char u : used) fb += u ? bd_block_doubles(L.bwin) * L.nblk * 8.0 : 0.0;
         const double Bd = B;
-        for (int k : {PG_PROF_FWD, PG_PROF_BWD}) {
+        for (int k : {BC == 32 ? PG_PROF_FWD_W : PG_PROF_FWD, BC == 32 ? PG_PROF_BWD_W : PG_PROF_BWD}) {
             ctx->prof_flops[k] += 2.0 * L.n * (double)L.bw * Bd;
             ctx->prof_bytes[k] += 16.0 * L.np * Bd + fb;
         }
@@ -1818,11 +1821,12 @@ extern "C" int pg_profile_read(pg_ctx* ctx, pg_kernel_profile* out, int n, int r
         pg_kernel_profile& b = out[PG_PROF_BAND];
         b.total_ms = b.alg_bytes = b.alg_flops = 0.0;
         b.launches = 0;
-        for (int k : {PG_PROF_FWD, PG_PROF_BWD, PG_PROF_BORDER, PG_PROF_FIX}) {
+        for (int k : {PG_PROF_FWD, PG_PROF_BWD, PG_PROF_FWD_W, PG_PROF_BWD_W, PG_PROF_BORDER,
+                      PG_PROF_FIX}) {
             b.total_ms += ctx->prof_ms[k];
             b.launches += ctx->prof_launches[k];
             b.alg_flops += ctx->prof_flops[k];
-            if (k == PG_PROF_FWD || k == PG_PROF_BWD) b.alg_bytes += ctx->prof_bytes[k];
+            if (k != PG_PROF_BORDER && k != PG_PROF_FIX) b.alg_bytes += ctx->prof_bytes[k];
         }
     }
     if (reset) {
