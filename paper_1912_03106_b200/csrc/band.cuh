@@ -1352,6 +1352,72 @@ k_band_rhs_dia(RhsDia a, const double* __restrict__ u_prev, const double* __rest
     }
 }
 
+// k_band_rhs_dia with the stencil width (UU upper diagonals) and the source
+// count (<= NS) fixed at compile time: no dummy loads, half the registers for
+// the source shapes, so 4 CTAs per SM stay resident (the generic kernel runs 3
+// at 80 registers and is latency-bound at 37 % warps active on the 511^2 grid,
+// profiles/r02c_ncu_rhs_dia_cfg4.json).  Same arithmetic, same order: bit-identical.
+template <int UU, int NS, int MINB, int CC>
+__global__ void __launch_bounds__(256, MINB)
+k_band_rhs_dia_t(RhsDia a, const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
+                 const double* __restrict__ src, const int* __restrict__ perm,
+                 double* __restrict__ Y) {
+    __shared__ int sp[CC];
+    __shared__ double sc[CC], ss[CC][NS];
+    const int gc0 = blockIdx.y * CC;
+    const int ncol = min(CC, a.B - gc0);
+    for (int t = threadIdx.x; t < CC * NS; t += blockDim.x) {
+        const int j = t / NS, q = t % NS;
+        const int b = j < ncol ? perm[gc0 + j] : 0;
+        if (q == 0) {
+            sp[j] = b;
+            sc[j] = j < ncol ? inv_dt[b] : 0.0;
+        }
+        ss[j][q] = (j < ncol && q < a.n_src) ? src[(size_t)b * a.n_src + q] : 0.0;
+    }
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.ldy) return;
+    if (i >= a.n) {
+        for (int j = 0; j < ncol; ++j) Y[(size_t)(gc0 + j) * a.ldy + i] = 0.0;
+        return;
+    }
+    double mup[UU], mlo[UU];
+    int oup[UU], olo[UU];
+    const double m0 = a.mk[i].x;
+#pragma unroll
+    for (int u = 0; u < UU; ++u) {
+        const int o = a.off[u + 1];
+        const bool hu = i + o < a.n, hl = i - o >= 0;
+        mup[u] = hu ? a.mk[(size_t)(u + 1) * a.n + i].x : 0.0;
+        mlo[u] = hl ? a.mk[(size_t)(u + 1) * a.n + i - o].x : 0.0;
+        oup[u] = hu ? o : 0;               // in-range dummy offset when absent
+        olo[u] = hl ? -o : 0;
+    }
+    double sh[NS];
+    bool has_src = false;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        sh[q] = q < a.n_src ? a.shapes[(size_t)q * a.n + i] : 0.0;
+        has_src |= sh[q] != 0.0;
+    }
+    double* yo = Y + (size_t)gc0 * a.ldy + i;
+#pragma unroll 4
+    for (int j = 0; j < ncol; ++j) {
+        const double* ub = u_prev + (size_t)sp[j] * a.n + i;
+        double v = m0 * ub[0];
+#pragma unroll
+        for (int u = 0; u < UU; ++u) v = fma(mup[u], ub[oup[u]], fma(mlo[u], ub[olo[u]], v));
+        // (the generic kernel adds 0 * u for its unused diagonals: exact zeros)
+        double f = 0.0;
+        if (has_src) {
+#pragma unroll
+            for (int q = 0; q < NS; ++q) f = fma(ss[j][q], sh[q], f);
+        }
+        yo[(size_t)j * a.ldy] = fma(sc[j], v, f);
+    }
+}
+
 // Same rhs, S-stage cp.async ring: the halos of the next S - 1 columns are in
 // flight (LDGSTS, zero-filled outside [0, n)) while column j is computed from
 // shared memory -- bytes in flight per CTA no longer depend on registers.

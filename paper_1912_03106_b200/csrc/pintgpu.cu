@@ -1452,7 +1452,9 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         for (int u = 1; u <= L.U; ++u) ra.off[u] = L.off[u];
         static const int rhs_sm = env_flag("PG_RHS_SM", 2);  // 0 = k_band_rhs_dia (A/B)
         const int ldh = (256 + 2 * L.omax + 255) / 256;        // halo loads per thread
-        if (rhs_sm == 2 && ldh <= 5) {
+        // (the 511^2 grid's 1,280-row halo per 256-row tile: direct gathers win,
+        // 8.3 vs 9.7 ms per 4,096 columns, round 2; PG_RHS_SM=3 forces the ring)
+        if ((rhs_sm == 2 && ldh <= 4) || (rhs_sm == 3 && ldh <= 5)) {
             // cp.async ring: 8 column slots (6 for the 511^2 grid's 1,278-row halo)
             dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
             const int S = ldh <= 4 ? 8 : 6;
@@ -1469,7 +1471,16 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             }
         } else {
             dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
-            k_band_rhs_dia<<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y);
+            // 7-point stencils with <= 4 sources: the compile-time variant at 5
+            // CTAs per SM (511^2, 4,096 columns: 6.5 ms against 8.3 ms generic and
+            // 9.7 ms for the cp.async ring; 4 / 6 CTAs per SM and 4 / 8 / 16
+            // columns per CTA measured slower).  PG_RHS_T=0: generic (A/B)
+            static const int rhs_t = env_flag("PG_RHS_T", 1);
+            if (L.U == 3 && L.n_src <= 4 && rhs_t)
+                k_band_rhs_dia_t<3, 4, 5, BD_RHS_CC><<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src,
+                                                                          d_perm, L.Y);
+            else
+                k_band_rhs_dia<<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y);
         }
     } else {
         k_band_rhs<<<gr, 256, 0, st>>>(L.n, L.np, B, L.row_ptr, L.col_idx, L.m_val, L.n_src,
