@@ -185,6 +185,18 @@ int  pg_fas_rhs(pg_ctx* ctx, int coarse, int coarsen, int B,
                 const double* kept, const double* cprop, const double* res,
                 double* rhs, int mode, void* stream);
 
+/* Row algebra of the level stores the engine keeps on the device (rows of n
+ * doubles; replaces the reference's BlockState add / subtract / copy loops,
+ * state.py:44-72, as used by mgrit.py:447-450, :483-490, :545-571):
+ *   out[ro(b)] = a[ra(b)]                       (c == NULL)
+ *   out[ro(b)] = a[ra(b)] + sign * c[rc(b)]     (sign = +1 or -1)
+ * for b = 0..B-1, row selectors r(b) = idx ? idx[b] : start + b * step
+ * (idx: device int32 [B] or NULL).  out may alias a or c row for row. */
+int  pg_rows_axpby(pg_ctx* ctx, int n, int B,
+                   const double* a, const int32_t* a_idx, int a_start, int a_step,
+                   const double* c, const int32_t* c_idx, int c_start, int c_step, int sign,
+                   double* out, const int32_t* o_idx, int o_start, int o_step, void* stream);
+
 /* Number of kernels this context has launched (for the bench). */
 int64_t pg_launch_count(pg_ctx* ctx);
 

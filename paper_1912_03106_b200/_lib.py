@@ -82,6 +82,9 @@ EXPORTS = {
                               c_void_p, c_void_p, c_void_p]),
     "pg_fas_rhs": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,
                            c_void_p, c_void_p, c_int, c_void_p]),
+    "pg_rows_axpby": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
+                              c_void_p, c_void_p, c_int, c_int, c_int,
+                              c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "pg_launch_count": (c_int64, [c_void_p]),
     "pg_profile": (c_int, [c_void_p, c_int]),
     "pg_profile_read": (c_int, [c_void_p, ctypes.POINTER(KernelProfile), c_int, c_int]),

@@ -133,3 +133,30 @@ __global__ void k_fas_rhs(int sf, int sc, int coarsen, int B, const double* __re
         rhs[k] = __dadd_rn(__dsub_rn(kept[k], cprop[k]), rr);
     }
 }
+
+// Row algebra of the engine's level stores (rows of n doubles):
+//   out[ro(b)] = a[ra(b)]                      (c == NULL)
+//   out[ro(b)] = a[ra(b)] + sgn * c[rc(b)]     (sgn = +1 / -1)
+// with r*(b) = idx ? idx[b] : start + b * step.  Covers the error payload
+// v - kept (mgrit.py:483-490, :545-560), the C-store seeding / correction
+// c_store (+)= e[C rows] (mgrit.py:447-450, :562-571) and strided F-point
+// views.  Plain IEEE add / subtract per entry; out may alias a or c row-wise.
+struct RowSel {
+    const int* idx;
+    int start, step;
+    __device__ __forceinline__ size_t row(int b) const {
+        return idx ? (size_t)idx[b] : (size_t)(start + (long long)b * step);
+    }
+};
+__global__ void k_rows_axpby(int n, int B, const double* __restrict__ a, RowSel ra,
+                             const double* c, RowSel rc, int sgn, double* out, RowSel ro) {
+    for (int b = blockIdx.y; b < B; b += gridDim.y) {
+        const double* ap = a + ra.row(b) * n;
+        const double* cp = c ? c + rc.row(b) * n : nullptr;
+        double* op = out + ro.row(b) * n;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            const double av = ap[i];
+            op[i] = cp ? (sgn > 0 ? __dadd_rn(av, cp[i]) : __dsub_rn(av, cp[i])) : av;
+        }
+    }
+}

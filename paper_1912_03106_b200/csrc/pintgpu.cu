@@ -1800,6 +1800,24 @@ extern "C" int pg_fas_rhs(pg_ctx* ctx, int coarse, int coarsen, int B, const dou
     return PG_OK;
 }
 
+extern "C" int pg_rows_axpby(pg_ctx* ctx, int n, int B, const double* a, const int32_t* a_idx,
+                             int a_start, int a_step, const double* c, const int32_t* c_idx,
+                             int c_start, int c_step, int sign, double* out,
+                             const int32_t* o_idx, int o_start, int o_step, void* stream) {
+    if (!ctx) return PG_EINVAL;
+    if (B <= 0 || n <= 0) return (B == 0 || n == 0) ? PG_OK : PG_EINVAL;
+    if (!a || !out) return set_err(ctx, PG_EINVAL, "null row operand");
+    if (c && sign != 1 && sign != -1) return set_err(ctx, PG_EINVAL, "sign must be +1 or -1");
+    CU(cudaSetDevice(ctx->device));
+    const int gx = std::max(1, std::min((n + 255) / 256, 64));
+    const int gy = std::min(B, 32768);
+    k_rows_axpby<<<dim3(gx, gy), 256, 0, (cudaStream_t)stream>>>(
+        n, B, a, RowSel{a_idx, a_start, a_step}, c, RowSel{c_idx, c_start, c_step}, sign, out,
+        RowSel{o_idx, o_start, o_step});
+    LAUNCHED();
+    return PG_OK;
+}
+
 #include "newton_host.inc"
 
 extern "C" int64_t pg_launch_count(pg_ctx* ctx) { return ctx ? ctx->launches : 0; }

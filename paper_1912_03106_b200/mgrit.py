@@ -200,6 +200,7 @@ class _Level:
         self.row_of_pt = torch.as_tensor(np.arange(self.n_points) - self.own_lo,
                                          dtype=torch.int32, device=dev)
         self.pt_idx = torch.arange(self.n_points, dtype=torch.int32, device=dev)
+        self.c_rows = torch.as_tensor(self.c_idx - self.own_lo, dtype=torch.int32, device=dev)
         # per F-offset tables (contiguous [K] / [K, n_src])
         self.inv_dt_off, self.src_off, self.gidx_off = {}, [{}, {}], {}
         self.inv_dt_off_h = {}
@@ -443,8 +444,7 @@ class MgritSolver:
                 nxt.rhs[lo - nxt.own_lo:hi - nxt.own_lo].copy_(b)
         nxt.use_rhs = True
         if nxt.K:
-            rows = torch.as_tensor(nxt.c_idx - nxt.own_lo, device=prob.device)
-            torch.index_select(nxt.u_keep, 0, rows, out=nxt.c_store)
+            prob.rows_axpby(nxt.K, nxt.c_store, nxt.u_keep, a_rows=nxt.c_rows)
 
     def _coarsest_solve(self, lvl, nested=False):
         """Gather, sequential on-device chain on rank 0, scatter
@@ -499,13 +499,13 @@ class MgritSolver:
         if nested:
             lvl.u_keep.copy_(mine)
         else:
-            lvl.u_keep.sub_(mine).neg_()                 # v - kept
+            prob.rows_axpby(lvl.n_owned, lvl.u_keep, mine, lvl.u_keep, sign=-1)   # v - kept
         if lvl.K:
-            rows = torch.as_tensor(lvl.c_idx - lvl.own_lo, device=dev)
             if nested:
-                torch.index_select(lvl.u_keep, 0, rows, out=lvl.c_store)
+                prob.rows_axpby(lvl.K, lvl.c_store, lvl.u_keep, a_rows=lvl.c_rows)
             else:
-                lvl.c_store.add_(lvl.u_keep.index_select(0, rows))
+                prob.rows_axpby(lvl.K, lvl.c_store, lvl.c_store, lvl.u_keep, sign=1,
+                                c_rows=lvl.c_rows)
 
     def _coarsest_chain(self, lvl, g, g_idx):
         """The serial chain v_i = Phi(v_{i-1}) (+ g_i) over the coarsest grid on
@@ -576,11 +576,12 @@ class MgritSolver:
                         cur = out
                     else:
                         cur = coarse.c_store
-                    view = coarse.u_keep[j - 1::m][:K]
+                    # rows j - 1, j - 1 + m, ... of u_keep: v (inject) or v - kept
                     if inject:
-                        view.copy_(cur)
+                        prob.rows_axpby(K, coarse.u_keep, cur, out_rows=(j - 1, m))
                     else:
-                        view.sub_(cur).neg_()
+                        prob.rows_axpby(K, coarse.u_keep, cur, coarse.u_keep, sign=-1,
+                                        out_rows=(j - 1, m), c_rows=(j - 1, m))
             # F-tail after the last owned C-point (mgrit.py:529-532)
             last_c = int(coarse.c_idx[-1]) if K else coarse.left_index
             if coarse.own_hi - 1 > last_c:
@@ -591,11 +592,12 @@ class MgritSolver:
                     self._phi_pts(coarse, v, i, i + 1, out,
                                   g=coarse.rhs if use_g else None,
                                   g_idx=coarse.row_of_pt[i:i + 1] if use_g else None)
-                    row = coarse.u_keep[i - coarse.own_lo]
+                    r = i - coarse.own_lo
                     if inject:
-                        row.copy_(out[0])
+                        coarse.u_keep[r].copy_(out[0])
                     else:
-                        row.sub_(out[0]).neg_()
+                        prob.rows_axpby(1, coarse.u_keep, out, coarse.u_keep, sign=-1,
+                                        out_rows=(r, 0), c_rows=(r, 0))
                     v = out
         self._deliver(coarse, fine, inject)
 
@@ -619,7 +621,7 @@ class MgritSolver:
             elif inject:
                 dst.copy_(payload)
             else:
-                dst.add_(payload)
+                prob.rows_axpby(b - a, dst, dst, payload, sign=1)
 
         for _, lo, hi in local:
             apply(lo, hi, coarse.u_keep[lo - coarse.own_lo:hi - coarse.own_lo])
@@ -741,8 +743,8 @@ class MgritSolver:
     # --- driver (mgrit.py:679-761) ---
     def _initialize_guess(self):
         for lvl in self.levels:
-            lvl.c_store.zero_()
-            lvl.c_store.add_(lvl.anchor)
+            if lvl.K:
+                self.problem.rows_axpby(lvl.K, lvl.c_store, lvl.anchor, a_rows=(0, 0))
             lvl.use_rhs = False
 
     def seed(self, trajectory):

@@ -278,6 +278,24 @@ class GpuFemProblem:
             _lib.ptr(last_f), _lib.ptr(inv_dt), _lib.ptr(loss), self._stream()),
             "pg_c_residual")
 
+    def rows_axpby(self, B, out, a, c=None, sign=1, out_rows=None, a_rows=None, c_rows=None):
+        """out[ro(b)] = a[ra(b)] (+ sign * c[rc(b)]) for b < B over rows of
+        equal length (2-D row-contiguous tensors, or one row).  A row selector
+        is None (row b), an int32 device index tensor, or a (start, step) pair."""
+        def sel(r):
+            if r is None:
+                return None, 0, 1
+            if isinstance(r, tuple):
+                return None, int(r[0]), int(r[1])
+            return r, 0, 0
+        ai, a0, a1 = sel(a_rows)
+        ci, c0, c1 = sel(c_rows)
+        oi, o0, o1 = sel(out_rows)
+        _lib.check(self.ctx, self.lib.pg_rows_axpby(
+            self.ctx, int(out.shape[-1]), int(B), _lib.ptr(a), _lib.ptr(ai), a0, a1,
+            _lib.ptr(c), _lib.ptr(ci), c0, c1, int(sign), _lib.ptr(out), _lib.ptr(oi), o0, o1,
+            self._stream()), "pg_rows_axpby")
+
     def fas_rhs(self, coarse_level, coarsen, kept, cprop, res, out):
         _lib.check(self.ctx, self.lib.pg_fas_rhs(
             self.ctx, int(coarse_level), int(bool(coarsen)), int(kept.shape[0]),

@@ -70,6 +70,20 @@ class CpuDoubleProblem:
                 du = (cb - last_f[b]) * inv_dt[b]
                 loss[b] = torch.dot(w, du * du)
 
+    def rows_axpby(self, B, out, a, c=None, sign=1, out_rows=None, a_rows=None, c_rows=None):
+        def row(t, r, b):
+            t2 = t if t.dim() == 2 else t.view(1, -1)
+            if r is None:
+                return t2[b]
+            if isinstance(r, tuple):
+                return t2[r[0] + b * r[1]]
+            return t2[int(r[b])]
+        for b in range(B):
+            v = row(a, a_rows, b).clone()
+            if c is not None:
+                v = v + row(c, c_rows, b) if sign > 0 else v - row(c, c_rows, b)
+            row(out, out_rows, b).copy_(v)
+
     def fas_rhs(self, coarse, coarsen, kept, cprop, res, out):
         for b in range(kept.shape[0]):
             rr = (torch.as_tensor(self.spatial.restrict_field(res[b].numpy(), coarse - 1))

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-for t in 32 16 8 4; do PG_RHS_CCT=$t timeout 600 python tools/probe_band.py cfg4 0:4096 2>&1 | tail -1 > gpurun_out/probe_rhs_cc$t.txt; done
+( time timeout 1500 python -m pytest tests -m gpu -q -x --deselect "tests/test_gpu_full.py::test_config5_phi_matches_oracle" ) > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
