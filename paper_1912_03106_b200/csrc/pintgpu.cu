@@ -1062,18 +1062,27 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
 
 // warp tiling (WM x WN x WK consumer warps) per column-group width; the
 // deepest operand ring that fits the 227 KB shared-memory limit
-template <int BC, int CW, int NCHK, bool FWD, int WM, int WN, int WK>
-static int launch_rb_t(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, cudaStream_t st) {
-    constexpr size_t lim = 232448 - 1024;
-    constexpr int NBUF = rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, 4>() <= lim ? 4
-                       : rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, 3>() <= lim ? 3 : 2;
+template <int BC, int CW, int NCHK, bool FWD, int WM, int WN, int WK, int NBUF>
+static int launch_rb_n(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, cudaStream_t st) {
     constexpr size_t sm = rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, NBUF>();
-    static_assert(sm <= lim, "k_band_rb shared memory");
     auto k = k_band_rb<BC, CW, NCHK, FWD, WM, WN, WK, NBUF>;
     CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k<<<grid, 32 * (WM * WN * WK + 1), sm, st>>>(sa);
     LAUNCHED();
     return PG_OK;
+}
+
+template <int BC, int CW, int NCHK, bool FWD, int WM, int WN, int WK>
+static int launch_rb_t(pg_ctx* ctx, const BandSolveArgs& sa, dim3 grid, cudaStream_t st) {
+    constexpr size_t lim = 232448 - 1024;
+    constexpr int NBUF = rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, 4>() <= lim ? 4
+                       : rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, 3>() <= lim ? 3 : 2;
+    static_assert(rb_smem_bytes<BC, CW, NCHK, WM, WN, WK, NBUF>() <= lim, "k_band_rb shared memory");
+    // PG_RB_NBUF=2: shallow operand ring (dev A/B: two CTAs per SM)
+    static const int cap = env_flag("PG_RB_NBUF", 4);
+    if (cap == 2 && NBUF > 2)
+        return launch_rb_n<BC, CW, NCHK, FWD, WM, WN, WK, 2>(ctx, sa, grid, st);
+    return launch_rb_n<BC, CW, NCHK, FWD, WM, WN, WK, NBUF>(ctx, sa, grid, st);
 }
 
 template <int BC, int CW, int NCHK, bool FWD>

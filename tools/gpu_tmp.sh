@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-( time timeout 1500 python -m pytest tests -m gpu -q -x --deselect "tests/test_gpu_full.py::test_config5_phi_matches_oracle" ) > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+PG_BAND_BC=16 PG_RB_ALT=1 PG_RB_NBUF=2 timeout 600 python tools/probe_band.py cfg4 0:4096 2>&1 | tail -1 > gpurun_out/probe_bc16_2cta.txt
+PG_BAND_BC=16 PG_RB_ALT=1 timeout 600 python tools/probe_band.py cfg4 0:4096 2>&1 | tail -1 > gpurun_out/probe_bc16_alt1.txt
+PG_BAND_BC=16 timeout 600 python tools/probe_band.py cfg4 0:4096 2>&1 | tail -1 > gpurun_out/probe_bc16.txt
+timeout 600 python -m pytest tests/test_gpu_dropin.py -q > gpurun_out/pytest_dropin.log 2>&1
