@@ -2,6 +2,5 @@
 mkdir -p gpurun_out
 ( time timeout 1500 python -m pytest tests -m gpu -q --durations=8 ) > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-( time timeout 1500 python bench.py ) > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 600 python tools/probe_breakdown.py cfg2 > gpurun_out/bd_cfg2.txt 2>&1
-PINTGPU_GRAPHS=0 timeout 600 python tools/probe_breakdown.py cfg2 > gpurun_out/bd_cfg2_nograph.txt 2>&1
+( time timeout 1800 python bench.py ) > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+( time timeout 1200 python bench.py --impl reference ) > gpurun_out/bench_ref.log 2> gpurun_out/bench_ref.err; echo "ref rc=$?" >> gpurun_out/bench_ref.err
