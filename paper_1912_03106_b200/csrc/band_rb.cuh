@@ -304,3 +304,172 @@ template <int BC, int CW, int NCHK, int WM, int WN, int WK, int NBUF>
 constexpr size_t rb_smem_bytes() {
     return RbShape<BC, CW, NCHK, WM, WN, WK, NBUF>::smem_doubles * sizeof(double);
 }
+
+// ---------------------------------------------------------------------------
+// Warp-per-column-group chain for narrow windows (the strip systems of
+// strips.cuh: W = h + 1 <= 64) -- the same recurrence and operand layout as
+// k_band_rb, mapped for chains whose block step is too short to amortise
+// CTA-wide barriers (k_band_rb spends 2.0 us per W = 64 step against a
+// 0.8 us DMMA floor).  A CTA is NWC consumer warps + one producer warp; every
+// consumer warp owns its own NCW columns and all 32 rows of the block
+// (4 x NCW/8 DMMA tiles), with a private window ring, so the consumer warps
+// never synchronise with each other: they only share the operand stream (one
+// TMA ring of pieces, full / empty mbarriers with NWC arrivals), which
+// therefore serves NCW NWC columns per byte; two warps per SM sub-partition
+// hide each other's fragment-load latency.  Ring slots are [column][36]
+// (rows contiguous, stride 4 mod 16: conflict-free B-fragment loads), so
+// b_{k+1} goes into its slot as 16-byte cp.async pieces straight from the
+// column-major Y while step k runs; y_k overwrites b_k.  One accumulator per
+// tile: acc = D^-1 b_k + (-(D^-1 L_win)) y_win.
+#define BD_WLD 36
+template <int CW, int NCHK, bool FWD, int NWC, int NCW, int NBUF>
+__global__ void __launch_bounds__(32 * (NWC + 1), 1)
+k_band_wcol(BandSolveArgs a) {
+    constexpr int NB = BD_NB, NRT = NCW / 8, LDR = BD_WLD;
+    constexpr int W = CW * NCHK, NSLOT = W / NB, NR = NSLOT + 2;
+    constexpr int PIECE = NB * (CW + 4) > NB * BD_PD ? NB * (CW + 4) : NB * BD_PD;
+    constexpr int NPB = 1 + NCHK, SLOT = NCW * LDR;
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t full[NBUF], empty[NBUF];
+    double* bufs = sm;
+    double* rings = bufs + (size_t)NBUF * PIECE;
+    const int4 ch = a.chunks[blockIdx.x];
+    const double* F = a.F[ch.x];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pch = a.p0 + blockIdx.y;
+    const int s0 = pch * a.q;
+    const int s1 = pch + 1 == a.P ? a.nblk : s0 + a.q;
+    const int nsteps = s1 - s0;
+    const size_t blk_doubles = (size_t)NB * (BD_PD + NCHK * (CW + 4));
+    auto blk_of = [&](int s) { return FWD ? s0 + s : s1 - 1 - s; };
+    auto slot_of = [&](int b) { return ((b % NR) + NR) % NR; };
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < NBUF; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], NWC);
+        }
+        mbar_fence_init();
+    }
+    for (int t = threadIdx.x; t < NWC * NR * SLOT; t += blockDim.x) rings[t] = 0.0;
+    __syncthreads();
+    if (warp == NWC) {
+        if (lane == 0) {
+            const int total = nsteps * NPB;
+            for (int P = 0; P < total; ++P) {
+                const int buf = P % NBUF, use = P / NBUF;
+                if (use > 0) {
+                    mbar_wait(&empty[buf], (use - 1) & 1);
+                    fence_proxy_async_smem();
+                }
+                const int s = P / NPB, j = P % NPB;
+                const double* src = F + (size_t)blk_of(s) * blk_doubles +
+                                    (j == 0 ? 0 : (size_t)NB * BD_PD + (size_t)(j - 1) * NB * (CW + 4));
+                const uint32_t bytes = (uint32_t)((j == 0 ? NB * BD_PD : NB * (CW + 4)) * 8);
+                mbar_arrive_expect_tx(&full[buf], bytes);
+                tma_load_1d(bufs + (size_t)buf * PIECE, src, bytes, &full[buf]);
+            }
+        }
+        return;
+    }
+    // ---------------- consumer warp: columns col0 .. col0 + NCW - 1 ----------------
+    double* ring = rings + (size_t)warp * NR * SLOT;
+    const int col0 = ch.y + NCW * warp;
+    const int ncol = max(0, min(NCW, ch.z - NCW * warp));
+    const int g = lane >> 2, q4 = lane & 3;
+    // b_s -> its ring slot: 16 lanes per column (16 bytes = 2 rows each), two
+    // columns per instruction
+    constexpr int NST = NCW / 2;
+    auto stage_b = [&](int s) {
+        const uint32_t dst = smem_u32(ring + (size_t)slot_of(blk_of(s)) * SLOT);
+        const size_t row = (size_t)NB * blk_of(s) + 2 * (lane & 15);
+#pragma unroll
+        for (int i = 0; i < NST; ++i) {
+            const int c = 2 * i + (lane >> 4);
+            const bool ok = c < ncol;
+            const double* srcp = a.Y + (size_t)(col0 + (ok ? c : 0)) * a.ldy + row;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                             dst + 8u * (uint32_t)(c * LDR + 2 * (lane & 15))),
+                         "l"(srcp), "r"(ok ? 16 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage_b(0);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    for (int s = 0; s < nsteps; ++s) {
+        const int k = blk_of(s);
+        if (s + 1 < nsteps) stage_b(s + 1);
+        double acc[4][NRT][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NRT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        double* bk = ring + (size_t)slot_of(k) * SLOT;
+        const int slot0 = slot_of(FWD ? k - NSLOT : k + 1);
+#pragma unroll
+        for (int j = 0; j < NPB; ++j) {
+            const int P = s * NPB + j;
+            const int buf = P % NBUF;
+            mbar_wait(&full[buf], (P / NBUF) & 1);
+            const double* pc = bufs + (size_t)buf * PIECE;
+            if (j == 0) {
+#pragma unroll
+                for (int u = 0; u < NB / 4; ++u) {
+                    const int kk = 4 * u + q4;
+                    double av[4], bv[NRT];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) av[mi] = pc[(8 * mi + g) * BD_PD + kk];
+#pragma unroll
+                    for (int ni = 0; ni < NRT; ++ni) bv[ni] = bk[(8 * ni + g) * LDR + kk];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                        for (int ni = 0; ni < NRT; ++ni)
+                            dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < CW / 4; ++u) {
+                    const int wi = (j - 1) * CW + 4 * u;
+                    int sl = slot0 + wi / NB;
+                    if (sl >= NR) sl -= NR;
+                    const double* wsl = ring + (size_t)sl * SLOT;
+                    const int kk = wi % NB + q4;
+                    double av[4], bv[NRT];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) av[mi] = -pc[(8 * mi + g) * (CW + 4) + 4 * u + q4];
+#pragma unroll
+                    for (int ni = 0; ni < NRT; ++ni) bv[ni] = wsl[(8 * ni + g) * LDR + kk];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                        for (int ni = 0; ni < NRT; ++ni)
+                            dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[buf]);
+        }
+        // y_k: over b_k in the ring, and out to Y
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NRT; ++ni)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int r = 8 * mi + g, cc = 8 * ni + 2 * q4 + h;
+                    const double y = acc[mi][ni][h];
+                    bk[cc * LDR + r] = y;
+                    if (cc < ncol) a.Y[(size_t)(col0 + cc) * a.ldy + NB * k + r] = y;
+                }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
+}
+
+template <int CW, int NCHK, int NWC, int NCW, int NBUF>
+constexpr size_t wcol_smem_bytes() {
+    constexpr int PIECE = BD_NB * (CW + 4) > BD_NB * BD_PD ? BD_NB * (CW + 4) : BD_NB * BD_PD;
+    return ((size_t)NBUF * PIECE + (size_t)NWC * (CW * NCHK / BD_NB + 2) * NCW * BD_WLD) * sizeof(double);
+}

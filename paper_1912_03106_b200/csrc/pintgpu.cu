@@ -10,6 +10,7 @@
 #include "band.cuh"
 #include "band_rb.cuh"
 #include "spike_gemm.cuh"
+#include "strips.cuh"
 #include "newton_nk.cuh"
 
 #include <algorithm>
@@ -69,6 +70,10 @@ struct Level {
     struct Group {
         std::vector<double> key; int* perm; int4* chunks; int nch; int BC;
         std::vector<int4> hch;            // host copy of the chunks
+        // strip solves: the same column groups with the strip system's factor
+        // ids, and the <= 64-column tiles of the separator GEMM
+        int4* schunks = nullptr; int4* stiles = nullptr; int n_stiles = 0;
+        int4* wchunks = nullptr; int n_wch = 0;      // <= 128-column groups (k_band_wcol)
     };
     std::unordered_map<uint64_t, std::vector<Group>> groups;
     Group tmp_group{};
@@ -102,6 +107,17 @@ struct Level {
     std::unordered_map<uint64_t, JacPre> jac_pre;
     double* kj = nullptr;          // [kj_cap][nnz] assembled Jacobian values
     int kj_cap = 0;
+    // strip solves of large structured grids (strips.cuh)
+    struct Strips {
+        StripGeo geo{};
+        Level* sys = nullptr;               // block-diagonal banded system of the strips
+        std::vector<int> fmap;              // factor of this level -> factor of sys
+        std::vector<double*> Sinv;          // per sys factor: (A^-1)_pp, [ldp][ldp]
+        double** d_Sinv = nullptr;
+        int sinv_cap = 0;
+        double *Y1 = nullptr, *Y2 = nullptr, *Gp = nullptr, *Xp = nullptr;
+        int cap_B = 0;
+    } strips;
     int* d_status = nullptr;
     // nonlinear iron elements
     int n_elem = 0;
@@ -339,7 +355,13 @@ static void free_level(Level& L) {
         if (sp.d_GB) cudaFree(sp.d_GB);
     }
     for (auto& kv : L.groups)
-        for (auto& gr : kv.second) { cudaFree(gr.perm); cudaFree(gr.chunks); }
+        for (auto& gr : kv.second) {
+            cudaFree(gr.perm);
+            cudaFree(gr.chunks);
+            if (gr.schunks) cudaFree(gr.schunks);
+            if (gr.stiles) cudaFree(gr.stiles);
+            if (gr.wchunks) cudaFree(gr.wchunks);
+        }
     L.groups.clear();
     double* nk[] = {L.nk_u, L.nk_F, L.nk_D, L.nk_rhs, L.nk_R, L.nk_Z, L.nk_P, L.nk_Q,
                     L.nk_TR, L.nk_FT, L.nk_E, L.nk_ET, L.nk_s};
@@ -348,6 +370,14 @@ static void free_level(Level& L) {
     if (L.nk_act) cudaFree(L.nk_act);
     if (L.nk_flag) cudaFree(L.nk_flag);
     if (L.kj) cudaFree(L.kj);
+    if (L.strips.sys) {
+        free_level(*L.strips.sys);
+        delete L.strips.sys;
+        L.strips.sys = nullptr;
+    }
+    for (double* p : L.strips.Sinv) if (p) cudaFree(p);
+    void* sp[] = {L.strips.d_Sinv, L.strips.Y1, L.strips.Y2, L.strips.Gp, L.strips.Xp};
+    for (void* p : sp) if (p) cudaFree(p);
 }
 
 extern "C" void pg_destroy(pg_ctx* ctx) {
@@ -387,14 +417,8 @@ extern "C" int pg_set_options(pg_ctx* ctx, const pg_solver_opts* o) {
     return PG_OK;
 }
 
-extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
-    if (!ctx || !d) return -1;
-    if (d->n < 1 || d->nnz < d->n || !d->row_ptr || !d->col_idx || !d->m_val || !d->k_val) {
-        set_err(ctx, PG_EINVAL, "level needs n >= 1 and a CSR with a diagonal");
-        return -1;
-    }
-    CU(cudaSetDevice(ctx->device));
-    Level L;
+// fills L from the descriptor (host analysis + uploads); 0 on success
+static int build_level(pg_ctx* ctx, const pg_level_desc* d, Level& L) {
     L.n = d->n;
     L.nnz = d->nnz;
     L.n_src = d->n_src;
@@ -569,6 +593,85 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
         if (d->k_pre_val && (rc = dev_upload(ctx, &L.k_pre, d->k_pre_val, (size_t)d->nnz)))
             return -1;
     }
+    return 0;
+}
+
+// Strip system of a structured linear level whose natural band is wide:
+// side = 8 (h + 1) - 1 (the nested grids 2^k - 1), h >= 7.  Builds the
+// permuted block-diagonal operator A_ss (strips padded to whole 32-row blocks
+// with identity rows) as a second, hidden banded level.
+static int build_strips(pg_ctx* ctx, const pg_level_desc* d, Level& L) {
+    static const int on = []{ const char* e = getenv("PG_STRIPS"); return e && e[0] ? atoi(e) : 1; }();
+    const int side = d->side, S = 8;
+    // (127^2 and below: the natural-order chains are faster, 3.2 vs 4.5 ms per
+    // 4,096 columns -- the gather / scatter passes and the dense separator GEMM
+    // outweigh the saved chain work)
+    if (!on || d->n_elem > 0 || side < 255 || (long long)side * side != d->n || (side + 1) % S) return 0;
+    const int h = (side + 1) / S - 1;
+    if (L.bw < side || !L.band_ok) return 0;           // not a natural-order grid stencil
+    StripGeo g{};
+    g.side = side; g.S = S; g.h = h;
+    g.rows = (side * h + 31) / 32 * 32;
+    g.n = d->n; g.ldn = L.np;
+    g.n_ss = S * g.rows;
+    g.n_pp = (S - 1) * side;
+    g.ldp = (g.n_pp + 127) / 128 * 128;
+    auto strip_of = [&](int i) -> long long {           // strip row, or -1 - separator index
+        const int y = i / side, x = i % side;
+        const int s = y / (h + 1), yl = y % (h + 1);
+        if (yl == h) return -1 - (long long)(s * side + x);
+        return (long long)s * g.rows + (long long)x * h + yl;
+    };
+    std::vector<int> rp(g.n_ss + 1, 0), ci;
+    std::vector<double> mv, kv;
+    ci.reserve((size_t)d->nnz + g.n_ss);
+    mv.reserve(ci.capacity());
+    kv.reserve(ci.capacity());
+    std::vector<std::pair<int, int>> row;               // (strip column, CSR entry)
+    for (int r = 0; r < g.n_ss; ++r) {
+        const int s = r / g.rows, q = r % g.rows;
+        if (q >= side * h) {                            // padding: identity row
+            ci.push_back(r); mv.push_back(0.0); kv.push_back(1.0);
+        } else {
+            const int x = q / h, yl = q % h;
+            const int i = (s * (h + 1) + yl) * side + x;
+            row.clear();
+            for (int e = d->row_ptr[i]; e < d->row_ptr[i + 1]; ++e) {
+                const long long c = strip_of(d->col_idx[e]);
+                if (c >= 0) row.push_back({(int)c, e});
+            }
+            std::sort(row.begin(), row.end());
+            for (auto& pe : row) {
+                ci.push_back(pe.first); mv.push_back(d->m_val[pe.second]); kv.push_back(d->k_val[pe.second]);
+            }
+        }
+        rp[r + 1] = (int)ci.size();
+    }
+    pg_level_desc sd{};
+    sd.n = g.n_ss; sd.nnz = (int)ci.size();
+    sd.row_ptr = rp.data(); sd.col_idx = ci.data(); sd.m_val = mv.data(); sd.k_val = kv.data();
+    sd.n_src = 0; sd.side = 0; sd.n_elem = 0;
+    Level* sys = new Level();
+    if (build_level(ctx, &sd, *sys) != 0 || !sys->band_ok || sys->np != g.n_ss) {
+        free_level(*sys);
+        delete sys;
+        return 0;                                       // no strips: the natural band solve stays
+    }
+    L.strips.geo = g;
+    L.strips.sys = sys;
+    return 0;
+}
+
+extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
+    if (!ctx || !d) return -1;
+    if (d->n < 1 || d->nnz < d->n || !d->row_ptr || !d->col_idx || !d->m_val || !d->k_val) {
+        set_err(ctx, PG_EINVAL, "level needs n >= 1 and a CSR with a diagonal");
+        return -1;
+    }
+    CU(cudaSetDevice(ctx->device));
+    Level L;
+    if (build_level(ctx, d, L) != 0) { free_level(L); return -1; }
+    if (build_strips(ctx, d, L) != 0) { free_level(L); return -1; }
     ctx->levels.push_back(L);
     return (int)ctx->levels.size() - 1;
 }
@@ -1363,7 +1466,9 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
                     const double* inv_dt_host, const double* src, double* u_out,
                     const double* g, const int* g_idx, cudaStream_t st,
                     const double* copy_src = nullptr, const int* sub = nullptr,
-                    const int* fid_all = nullptr) {
+                    const int* fid_all = nullptr, Level::Group** rhs_only = nullptr) {
+    // rhs_only: stop after the right-hand sides are in L.Y (natural rows,
+    // grouped columns) and hand the column grouping back (strip solves)
     // fid_all (preconditioner mode): factor of every full-batch column, chosen
     // by the caller (frozen-Jacobian preconditioners) instead of by 1/dt
     std::vector<double> c(B);
@@ -1497,6 +1602,10 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     }
     LAUNCHED();
     if ((rc = prof_mark(ctx, PG_PROF_RHS, st))) return rc;
+    if (rhs_only) {
+        *rhs_only = grp;
+        return PG_OK;
+    }
     // finest partition (8, 4, 2 chunks) whose chunk CTAs fit one wave; none:
     // the plain chains (the column groups already cover the SMs)
     int pi = -1;
@@ -1588,6 +1697,205 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     return PG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Strip solve (strips.cuh) of a batch large enough to fill the GPU.
+
+// factor of the strip system and S^-1 = (A^-1)_pp for factor f of the level:
+// the separator unit vectors are solved with the level's own natural-order
+// banded factor, 512 columns at a time
+static int strips_factor(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
+    Level::Strips& T = L.strips;
+    Level& Sy = *T.sys;
+    if ((int)T.fmap.size() <= f) T.fmap.resize(L.FL.size(), -1);
+    if (T.fmap[f] >= 0) return PG_OK;
+    const double c = L.fac_c[f];
+    int sf = -1, rc;
+    if ((rc = factor_ids(ctx, Sy, &c, 1, &sf, st))) return rc;
+    if ((int)T.Sinv.size() <= sf) T.Sinv.resize(sf + 1, nullptr);
+    const StripGeo& g = T.geo;
+    const size_t sbytes = (size_t)g.ldp * g.ldp * sizeof(double);
+    CU(cudaMalloc(&T.Sinv[sf], sbytes));
+    CU(cudaMemsetAsync(T.Sinv[sf], 0, sbytes, st));
+    const int CH = 512;
+    double *E = nullptr, *X = nullptr, *dc = nullptr;
+    struct Tmp {
+        double *&a, *&b, *&c;
+        ~Tmp() { if (a) cudaFree(a); if (b) cudaFree(b); if (c) cudaFree(c); }
+    } tmp{E, X, dc};
+    CU(cudaMalloc(&E, (size_t)CH * g.n * sizeof(double)));
+    CU(cudaMalloc(&X, (size_t)CH * g.n * sizeof(double)));
+    CU(cudaMalloc(&dc, CH * sizeof(double)));
+    std::vector<double> hc(CH, c);
+    std::vector<int> ident(CH);
+    for (int j = 0; j < CH; ++j) ident[j] = j;
+    CU(cudaMemcpyAsync(dc, hc.data(), CH * sizeof(double), cudaMemcpyHostToDevice, st));
+    for (int j0 = 0; j0 < g.n_pp; j0 += CH) {
+        const int nj = std::min(CH, g.n_pp - j0);
+        k_strip_units<<<dim3(64, nj), 256, 0, st>>>(g, j0, nj, E);
+        LAUNCHED();
+        L.tmp_sub.clear();
+        if ((rc = band_phi(ctx, L, nj, nullptr, dc, hc.data(), nullptr, X, nullptr, nullptr, st, E,
+                           ident.data())))
+            return rc;
+        k_strip_sinv_rows<<<dim3((g.ldp + 255) / 256, nj), 256, 0, st>>>(g, j0, nj, X, T.Sinv[sf]);
+        LAUNCHED();
+    }
+    CU(cudaStreamSynchronize(st));                       // hc / ident / temporaries leave scope
+    if ((int)T.Sinv.size() > T.sinv_cap) {
+        if (T.d_Sinv) cudaFree(T.d_Sinv);
+        T.sinv_cap = std::max(64, 2 * (int)T.Sinv.size());
+        CU(cudaMalloc(&T.d_Sinv, T.sinv_cap * sizeof(double*)));
+    }
+    CU(cudaMemcpy(T.d_Sinv, T.Sinv.data(), T.Sinv.size() * sizeof(double*), cudaMemcpyHostToDevice));
+    T.fmap[f] = sf;
+    return PG_OK;
+}
+
+static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* inv_dt,
+                     const double* inv_dt_host, const double* src, double* u_out,
+                     const double* g, const int* g_idx, cudaStream_t st) {
+    Level::Strips& T = L.strips;
+    Level& Sy = *T.sys;
+    const StripGeo& geo = T.geo;
+    int rc;
+    // right-hand sides in natural order (grouped columns) + the grouping
+    Level::Group* grp = nullptr;
+    if ((rc = band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st, nullptr,
+                       nullptr, nullptr, &grp)))
+        return rc;
+    const int BC = grp->BC;
+    if (!grp->schunks) {
+        // the same column groups with the strip system's factor ids, and the
+        // <= 64-column tiles of the separator GEMM (per factor)
+        for (const int4& q : grp->hch)
+            if ((rc = strips_factor(ctx, L, q.x, st))) return rc;
+        // (the separator solves above went through L.Y: form the rhs again)
+        if ((rc = band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st,
+                           nullptr, nullptr, nullptr, &grp)))
+            return rc;
+        std::vector<int4> sch(grp->hch), tiles, wch;
+        for (int4& q : sch) q.x = T.fmap[q.x];
+        for (size_t i = 0; i < sch.size();) {
+            size_t j = i;
+            while (j < sch.size() && sch[j].x == sch[i].x) ++j;
+            const int c0 = sch[i].y, nc = sch[j - 1].y + sch[j - 1].z - c0;
+            for (int c = 0; c < nc; c += SG_TN)
+                tiles.push_back(make_int4(sch[i].x, c0 + c, std::min(SG_TN, nc - c), 0));
+            for (int c = 0; c < nc; c += 128)
+                wch.push_back(make_int4(sch[i].x, c0 + c, std::min(128, nc - c), 0));
+            i = j;
+        }
+        CU(cudaMalloc(&grp->wchunks, wch.size() * sizeof(int4)));
+        CU(cudaMemcpy(grp->wchunks, wch.data(), wch.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        grp->n_wch = (int)wch.size();
+        CU(cudaMalloc(&grp->schunks, sch.size() * sizeof(int4)));
+        CU(cudaMalloc(&grp->stiles, tiles.size() * sizeof(int4)));
+        CU(cudaMemcpy(grp->schunks, sch.data(), sch.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(grp->stiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        grp->n_stiles = (int)tiles.size();
+    }
+    if (B > T.cap_B) {
+        void* old[] = {T.Y1, T.Y2, T.Gp, T.Xp};
+        for (void* p : old) if (p) cudaFree(p);
+        T.Y1 = T.Y2 = T.Gp = T.Xp = nullptr;
+        T.cap_B = B;
+        CU(cudaMalloc(&T.Y1, (size_t)B * geo.n_ss * sizeof(double)));
+        CU(cudaMalloc(&T.Y2, (size_t)B * geo.n_ss * sizeof(double)));
+        CU(cudaMalloc(&T.Gp, (size_t)B * geo.ldp * sizeof(double)));
+        CU(cudaMalloc(&T.Xp, (size_t)B * geo.ldp * sizeof(double)));
+    }
+    const int xt = (geo.side + 31) / 32;
+    const size_t tsm = (size_t)geo.h * 33 * sizeof(double);
+    if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
+    k_strip_gather<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, L.Y, T.Y1, T.Y2);
+    LAUNCHED();
+    if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
+    // chains of the strip system: window h + 1, unpartitioned, no fused scatter
+    const size_t sm = band_solve_smem(Sy, BC);
+    static const int wcol = env_flag("PG_STRIP_WCOL", 1);      // 0: k_band_rb chains (A/B)
+    auto solve = [&](double* Y) -> int {
+        BandSolveArgs sa{Sy.np, Sy.bwin, Sy.LDA, Sy.nblk, Sy.np, 0, Y, grp->schunks, Sy.d_FL,
+                         Sy.nblk, 1, 0, 0, {}};
+        for (int dir = 0; dir < 2; ++dir) {
+            const bool fwd = dir == 0;
+            sa.F = fwd ? Sy.d_FL : Sy.d_FU;
+            const int pk = fwd ? PG_PROF_FWD_W : PG_PROF_BWD_W;
+            int r;
+            if ((r = prof_mark(ctx, pk, st))) return r;
+            if (wcol && (Sy.bwin == 64 || Sy.bwin == 32)) {
+                // one CTA per (128-column group, strip): the strips are the
+                // chunks of an exact partition (no coupling across them)
+                sa.chunks = grp->wchunks;
+                sa.q = geo.rows / BD_NB;
+                sa.P = geo.S;
+                dim3 grid(grp->n_wch, geo.S);
+#define PG_WCOL(CW_, FWD_)                                                                  \
+    do {                                                                                    \
+        constexpr size_t wsm = wcol_smem_bytes<CW_, 1, 8, 16, 4>();                         \
+        SMEM_ATTR_ONCE((k_band_wcol<CW_, 1, FWD_, 8, 16, 4>), wsm);                         \
+        k_band_wcol<CW_, 1, FWD_, 8, 16, 4><<<grid, 288, wsm, st>>>(sa);                    \
+    } while (0)
+                if (Sy.bwin == 64) {
+                    if (fwd) PG_WCOL(64, true); else PG_WCOL(64, false);
+                } else {
+                    if (fwd) PG_WCOL(32, true); else PG_WCOL(32, false);
+                }
+#undef PG_WCOL
+                LAUNCHED();
+                sa.chunks = grp->schunks;
+                sa.q = Sy.nblk;
+                sa.P = 1;
+            } else if ((r = band_dir(ctx, Sy, BC, fwd, sa, dim3(grp->nch, 1), sm, st))) {
+                return r;
+            }
+            if ((r = prof_mark(ctx, pk, st))) return r;
+        }
+        return PG_OK;
+    };
+    if ((rc = solve(T.Y1))) return rc;
+    const int gy = std::min(B, 16384);
+    if ((rc = prof_mark(ctx, PG_PROF_FIX, st))) return rc;
+    k_strip_g<<<dim3((geo.ldp + 255) / 256, gy), 256, 0, st>>>(
+        geo, B, L.row_ptr, L.col_idx, L.m_val, L.k_val, inv_dt, grp->perm, L.Y, T.Y1, T.Gp);
+    LAUNCHED();
+    SMEM_ATTR_ONCE(k_strip_sinv_gemm, SG_SMEM);
+    k_strip_sinv_gemm<<<dim3(geo.ldp / SG_TM, 1, grp->n_stiles), 256, SG_SMEM, st>>>(
+        geo.ldp, T.d_Sinv, T.Gp, T.Xp, grp->stiles);
+    LAUNCHED();
+    k_strip_update<<<dim3((2 * (geo.S - 1) * geo.side + 255) / 256, gy), 256, 0, st>>>(
+        geo, B, L.row_ptr, L.col_idx, L.m_val, L.k_val, inv_dt, grp->perm, T.Xp, T.Y2);
+    LAUNCHED();
+    if ((rc = prof_mark(ctx, PG_PROF_FIX, st))) return rc;
+    if ((rc = solve(T.Y2))) return rc;
+    if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
+    k_strip_scatter<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, T.Y2, T.Xp, grp->perm, u_out, g,
+                                                         g_idx);
+    LAUNCHED();
+    if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
+    if (ctx->prof_on) {
+        // algorithmic work stays the reference's dpbtrs (2 n w per direction and
+        // column): the strips do the same solve with fewer operations
+        const double Bd = B;
+        for (int k : {PG_PROF_FWD_W, PG_PROF_BWD_W}) {
+            ctx->prof_flops[k] += 2.0 * L.n * (double)L.bw * Bd;
+            ctx->prof_bytes[k] += 2.0 * 16.0 * geo.n_ss * Bd;
+        }
+        ctx->prof_bytes[PG_PROF_RHS] += 8.0 * (L.n + L.np) * Bd;
+        ctx->prof_bytes[PG_PROF_SCATTER] += (8.0 * L.np + 16.0 * geo.n_ss + 8.0 * geo.n_ss + 8.0 * L.n) * Bd;
+        ctx->prof_flops[PG_PROF_FIX] += 2.0 * (double)geo.n_pp * geo.n_pp * Bd;
+        CU(cudaStreamSynchronize(st));
+        for (int k = 0; k + 1 < ctx->ev_used; k += 2) {
+            float ms = 0.f;
+            CU(cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]));
+            ctx->prof_ms[ctx->ev_kind[k]] += ms;
+            ctx->prof_launches[ctx->ev_kind[k]] += 1;
+        }
+        ctx->ev_used = 0;
+        ctx->ev_kind.clear();
+    }
+    return PG_OK;
+}
+
 // Jacobi-PCG columns that stopped at max_iters above rtol make the call fail
 // (PG_ENOCONV): the engine must not accept an unconverged Phi.  The direct
 // solve of the reference (problems.py:130-146) cannot fail this way.
@@ -1665,6 +1973,9 @@ extern "C" int pg_phi_batch_h(pg_ctx* ctx, int level, int B, const double* u_pre
         LAUNCHED();
         return PG_OK;
     } else if (ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok) {
+        // batches that fill the GPU with 32-column groups: the strip solve
+        if (L.strips.sys && B >= 26 * ctx->n_sm && band_rb_on())
+            return strip_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
         return band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
     } else if (L.resident) {
         if ((rc = launch_resident(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st)))
