@@ -88,8 +88,11 @@ def workload_config(spec, world):
         "spatial_strategy": mg["spatial_strategy"],
         "n_spatial_grids": spec["n_spatial_grids"],
         "tolerance": mg["tolerance"],
-        "inner_solver": "banded Cholesky (reference algorithm), fp64 DMMA solves; factors "
-                        f"shared within dt_merge_rtol {spec['inner'].get('dt_merge_rtol', 0.0)}",
+        "inner_solver": "banded Cholesky (direct), fp64 DMMA solves; 4,096-column batches by the "
+                        "strip solve (8 strips + separator Schur complement: the same direct "
+                        "solve, 2.7x fewer flops), smaller batches in the reference's natural "
+                        "order; factors shared within dt_merge_rtol "
+                        f"{spec['inner'].get('dt_merge_rtol', 0.0)}",
         "parallelism": f"time-parallel C-intervals over {world} GPU(s)",
         "l2": "working set > L2 (level-0 batch vectors 8.6 GB each); no flush needed",
     }
@@ -540,6 +543,25 @@ def run_b200(args):
     prof = problem.profile_read(reset=True)
     problem.profile(False)
 
+    # --- the same solve with the natural-order band solve (the reference's
+    # dpbtrs ordering) instead of the strip solve: one solve, its time and how
+    # far the two direct solvers' residual histories are apart
+    natural = None
+    if getattr(problem, "opts", None) is not None and problem.opts.strips and not args.no_natural:
+        problem.use_strips(False)
+        barrier()
+        e0.record(stream)
+        run_n, _ = solver.solve(gather_solution=False)
+        e1.record(stream)
+        barrier()
+        problem.use_strips(True)
+        hn, hs = np.array(_history(run_n)), np.array(_history(runs[-1]))
+        natural = {"time_to_solution_s": max_over_ranks(e0.elapsed_time(e1) / 1e3),
+                   "iterations": run_n.iterations, "residual_history": list(map(float, hn)),
+                   "same_iterations_as_strip_solve": bool(run_n.iterations == runs[-1].iterations),
+                   "max_rel_history_diff_vs_strip_solve":
+                       float(np.max(np.abs(hn - hs) / hn)) if len(hn) == len(hs) else None}
+
     # --- GPU sequential time stepping on a window of the horizon
     # (extrapolated: 2^16 dependent single-column Phi calls take minutes)
     seq = None
@@ -630,8 +652,8 @@ def run_b200(args):
         if wide and tr and tr.get("workload") == "cfg4-headline":
             traffic = tr.get("dram_bytes_per_launch")
         roofline = {"bound": "tensor",
-                    "kernel": ("k_band_rb<32, ...> (band chains of the 4,096-column level-0 "
-                               "batches, fwd + bwd)" if wide else
+                    "kernel": ("k_band_wcol<64, 1, ...> (strip-system band chains of the "
+                               "4,096-column level-0 batches, 2 solves x fwd + bwd)" if wide else
                                "band chains (k_band_rb / k_band_chain_ks, fwd + bwd)"),
                     "achieved": fl / (ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
                     "frac": fl / (ms * 1e-3) / 1e12 / fpk, "traffic": traffic,
@@ -643,9 +665,10 @@ def run_b200(args):
                     "hbm_achieved_gbs": by / (ms * 1e-3) / 1e9, "hbm_peak_gbs": peak,
                     "hbm_frac": by / (ms * 1e-3) / 1e9 / peak,
                     "hbm_peak_source": peak_src,
-                    "alg_model": "flops 2 n w per direction and column (w = the band's lower "
-                                 "bandwidth: the reference's dpbtrs); bytes = Y in/out + each "
-                                 "distinct factor once",
+                    "alg_model": "flops 2 n w per direction, column and solve (n, w = size and "
+                                 "lower bandwidth of the banded systems the kernel solves: "
+                                 "dpbtrs; strip systems n = 257,792, w = 64); bytes = Y "
+                                 "in/out + each distinct factor once",
                     "timing": "CUDA events around every launch in a separate profiling solve "
                               f"({prof_elapsed:.2f} s with its per-call syncs)",
                     "kernels": kernels}
@@ -667,13 +690,16 @@ def run_b200(args):
                   "phi_columns_per_solve": r.phi_columns, "phi_calls_per_solve": r.phi_calls,
                   "parity": "no CPU reference run at this size (days of CPU); pinned by "
                             "tests/golden/mgrit_cfg4shape_n128.npz (4-level cycle, reference "
-                            "engine) and the 511^2 Phi tests (test_gpu_phi.py)"},
+                            "engine; natural-order and strip solve, tests/test_gpu_full.py, "
+                            "test_gpu_strips.py), the 511^2 Phi tests and the "
+                            "natural_band_solve leg of this line"},
         "e2e": {"value": n_steps * n0 / e2e_s, "unit": "fine time-step*DOF/s",
                 "seconds": e2e_s, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h,
                 "parts": {k: round(v, 4) for k, v in e2e_parts.items()},
                 "reps_s": [round(x[0], 4) for x in e2e_runs],
                 "stat": "median of the repetitions in reps_s"},
         "roofline": roofline,
+        "natural_band_solve": natural,
         "sequential_gpu": seq,
         "config2": cfg2,
         "config3": cfg3,
@@ -721,6 +747,8 @@ def main():
     ap.add_argument("--e2e-reps", type=int, default=1,
                     help="end-to-end repetitions (median reported)")
     ap.add_argument("--no-seq", action="store_true", help="skip the GPU sequential-stepping leg")
+    ap.add_argument("--no-natural", action="store_true",
+                    help="skip the natural-order band-solve leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)          # rank 0 only, host cores

@@ -98,6 +98,14 @@ typedef struct pg_solver_opts {
                                    existing 1/dt within this relative
                                    distance (0 = the reference's bitwise
                                    (level, float(dt)) cache key)           */
+    int32_t strips;             /* banded Cholesky on structured grids of
+                                   255^2 and more, batches that fill the GPU:
+                                   1 = strip solve (strips + separator Schur
+                                   complement: the same direct solve with
+                                   ~2.7x fewer flops, agrees with the
+                                   natural-order solve to rounding), 0 = the
+                                   natural-order band solve only (the
+                                   reference's dpbtrs ordering)            */
 } pg_solver_opts;
 
 /* Per-call statistics (host struct). */

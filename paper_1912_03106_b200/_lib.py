@@ -45,6 +45,7 @@ class SolverOpts(ctypes.Structure):
         ("damping", c_double), ("max_halvings", c_int32),
         ("nu0", c_double), ("k1", c_double), ("k2", c_double), ("k3", c_double),
         ("dt_merge_rtol", c_double),
+        ("strips", c_int32),
     ]
 
 

@@ -115,7 +115,7 @@ struct Level {
         std::vector<double*> Sinv;          // per sys factor: (A^-1)_pp, [ldp][ldp]
         double** d_Sinv = nullptr;
         int sinv_cap = 0;
-        double *Y1 = nullptr, *Y2 = nullptr, *Gp = nullptr, *Xp = nullptr;
+        double *Y1 = nullptr, *Gp = nullptr, *Xp = nullptr;   // one strip-ordered buffer
         int cap_B = 0;
     } strips;
     int* d_status = nullptr;
@@ -323,6 +323,7 @@ extern "C" int pg_create(pg_ctx** out, int device) {
     ctx->opts.k2 = 0.0;
     ctx->opts.k3 = 1.0;
     ctx->opts.inner = PG_INNER_PCG;
+    ctx->opts.strips = 1;
     if (cudaMalloc(&ctx->d_iters, 2 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&ctx->d_ictr, 3 * sizeof(int)) != cudaSuccess ||
         cudaMemset(ctx->d_iters, 0, 2 * sizeof(unsigned long long)) != cudaSuccess ||
@@ -376,7 +377,7 @@ static void free_level(Level& L) {
         L.strips.sys = nullptr;
     }
     for (double* p : L.strips.Sinv) if (p) cudaFree(p);
-    void* sp[] = {L.strips.d_Sinv, L.strips.Y1, L.strips.Y2, L.strips.Gp, L.strips.Xp};
+    void* sp[] = {L.strips.d_Sinv, L.strips.Y1, L.strips.Gp, L.strips.Xp};
     for (void* p : sp) if (p) cudaFree(p);
 }
 
@@ -606,7 +607,10 @@ static int build_strips(pg_ctx* ctx, const pg_level_desc* d, Level& L) {
     // (127^2 and below: the natural-order chains are faster, 3.2 vs 4.5 ms per
     // 4,096 columns -- the gather / scatter passes and the dense separator GEMM
     // outweigh the saved chain work)
-    if (!on || d->n_elem > 0 || side < 255 || (long long)side * side != d->n || (side + 1) % S) return 0;
+    static const int min_side = []{ const char* e = getenv("PG_STRIPS_MIN_SIDE"); return e && e[0] ? atoi(e) : 255; }();
+    if (!on || d->n_elem > 0 || side < min_side || side < 63 || (long long)side * side != d->n ||
+        (side + 1) % S)
+        return 0;
     const int h = (side + 1) / S - 1;
     if (L.bw < side || !L.band_ok) return 0;           // not a natural-order grid stencil
     StripGeo g{};
@@ -1795,19 +1799,18 @@ static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
         grp->n_stiles = (int)tiles.size();
     }
     if (B > T.cap_B) {
-        void* old[] = {T.Y1, T.Y2, T.Gp, T.Xp};
+        void* old[] = {T.Y1, T.Gp, T.Xp};
         for (void* p : old) if (p) cudaFree(p);
-        T.Y1 = T.Y2 = T.Gp = T.Xp = nullptr;
+        T.Y1 = T.Gp = T.Xp = nullptr;
         T.cap_B = B;
         CU(cudaMalloc(&T.Y1, (size_t)B * geo.n_ss * sizeof(double)));
-        CU(cudaMalloc(&T.Y2, (size_t)B * geo.n_ss * sizeof(double)));
         CU(cudaMalloc(&T.Gp, (size_t)B * geo.ldp * sizeof(double)));
         CU(cudaMalloc(&T.Xp, (size_t)B * geo.ldp * sizeof(double)));
     }
     const int xt = (geo.side + 31) / 32;
     const size_t tsm = (size_t)geo.h * 33 * sizeof(double);
     if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
-    k_strip_gather<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, L.Y, T.Y1, T.Y2);
+    k_strip_gather<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, L.Y, T.Y1, nullptr);
     LAUNCHED();
     if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
     // chains of the strip system: window h + 1, unpartitioned, no fused scatter
@@ -1862,13 +1865,20 @@ static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
     k_strip_sinv_gemm<<<dim3(geo.ldp / SG_TM, 1, grp->n_stiles), 256, SG_SMEM, st>>>(
         geo.ldp, T.d_Sinv, T.Gp, T.Xp, grp->stiles);
     LAUNCHED();
-    k_strip_update<<<dim3((2 * (geo.S - 1) * geo.side + 255) / 256, gy), 256, 0, st>>>(
-        geo, B, L.row_ptr, L.col_idx, L.m_val, L.k_val, inv_dt, grp->perm, T.Xp, T.Y2);
-    LAUNCHED();
     if ((rc = prof_mark(ctx, PG_PROF_FIX, st))) return rc;
-    if ((rc = solve(T.Y2))) return rc;
+    // second solve on b_s - A_sp x_p: the strip buffer is re-gathered from the
+    // natural right-hand sides (one strip-ordered buffer instead of two: 8.4 GB
+    // at 511^2 x 4,096 columns)
     if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
-    k_strip_scatter<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, T.Y2, T.Xp, grp->perm, u_out, g,
+    k_strip_gather<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, L.Y, T.Y1, nullptr);
+    LAUNCHED();
+    k_strip_update<<<dim3((2 * (geo.S - 1) * geo.side + 255) / 256, gy), 256, 0, st>>>(
+        geo, B, L.row_ptr, L.col_idx, L.m_val, L.k_val, inv_dt, grp->perm, T.Xp, T.Y1);
+    LAUNCHED();
+    if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
+    if ((rc = solve(T.Y1))) return rc;
+    if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
+    k_strip_scatter<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, T.Y1, T.Xp, grp->perm, u_out, g,
                                                          g_idx);
     LAUNCHED();
     if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
@@ -1876,9 +1886,16 @@ static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
         // algorithmic work stays the reference's dpbtrs (2 n w per direction and
         // column): the strips do the same solve with fewer operations
         const double Bd = B;
+        // chains: two solves of the strip systems per call; algorithmic flops =
+        // the dpbtrs count of the systems actually solved (2 n_ss (h + 1) per
+        // direction, column and solve), bytes = Y in / out + the factors once
+        std::vector<char> used(Sy.FL.size(), 0);
+        for (const int4& q : grp->hch) used[T.fmap[q.x]] = 1;
+        double fb = 0.0;
+        for (char u : used) fb += u ? bd_block_doubles(Sy.bwin) * Sy.nblk * 8.0 : 0.0;
         for (int k : {PG_PROF_FWD_W, PG_PROF_BWD_W}) {
-            ctx->prof_flops[k] += 2.0 * L.n * (double)L.bw * Bd;
-            ctx->prof_bytes[k] += 2.0 * 16.0 * geo.n_ss * Bd;
+            ctx->prof_flops[k] += 2.0 * (2.0 * geo.n_ss * (double)Sy.bw * Bd);
+            ctx->prof_bytes[k] += 2.0 * (16.0 * geo.n_ss * Bd + fb);
         }
         ctx->prof_bytes[PG_PROF_RHS] += 8.0 * (L.n + L.np) * Bd;
         ctx->prof_bytes[PG_PROF_SCATTER] += (8.0 * L.np + 16.0 * geo.n_ss + 8.0 * geo.n_ss + 8.0 * L.n) * Bd;
@@ -1974,7 +1991,11 @@ extern "C" int pg_phi_batch_h(pg_ctx* ctx, int level, int B, const double* u_pre
         return PG_OK;
     } else if (ctx->opts.inner == PG_INNER_CHOLESKY && L.band_ok) {
         // batches that fill the GPU with 32-column groups: the strip solve
-        if (L.strips.sys && B >= 26 * ctx->n_sm && band_rb_on())
+        // (PG_STRIPS_MIN_B / PG_STRIPS_MIN_SIDE: test overrides -- the parity
+        // tests push the strip solve through the small reference fixtures)
+        static const int strips_min_b = env_flag("PG_STRIPS_MIN_B", 0);
+        if (L.strips.sys && ctx->opts.strips && band_rb_on() &&
+            B >= (strips_min_b > 0 ? strips_min_b : 26 * ctx->n_sm))
             return strip_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
         return band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
     } else if (L.resident) {

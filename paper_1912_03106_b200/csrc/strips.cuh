@@ -43,7 +43,7 @@ __device__ __forceinline__ int nat_to_strip(const StripGeo& g, int i) {
     return s * g.rows + x * g.h + yl;
 }
 
-// Y1 = Y2 = strip-ordered copy of the natural columns (padding rows 0).
+// Y1 (= Y2 when given) = strip-ordered copy of the natural columns (padding rows 0).
 // CTA = (strip s, 32 x-values): h natural row segments of 32 doubles in,
 // 32 h contiguous doubles out, transposed through shared memory.
 // grid (ceil(side / 32) * S, columns), 256 threads; smem h * 33 doubles
@@ -65,14 +65,14 @@ k_strip_gather(StripGeo g, const double* __restrict__ Yn, double* __restrict__ Y
         const int xl = t / g.h, yl = t - xl * g.h;
         const double v = tile[yl * 33 + xl];
         Y1[base + t] = v;
-        Y2[base + t] = v;
+        if (Y2) Y2[base + t] = v;
     }
     // padding rows of the strip (written by the CTA of its last x tile)
     if (x0 + 32 >= g.side) {
         const size_t pb = col * g.n_ss + (size_t)s * g.rows + (size_t)g.side * g.h;
         for (int t = threadIdx.x; t < g.rows - g.side * g.h; t += 256) {
             Y1[pb + t] = 0.0;
-            Y2[pb + t] = 0.0;
+            if (Y2) Y2[pb + t] = 0.0;
         }
     }
 }

@@ -143,7 +143,7 @@ class GpuOperatorProblem(GpuFemProblem):
             inner=_lib.PG_INNER_CHOLESKY if inner == "cholesky" else _lib.PG_INNER_PCG,
             rtol=float(rtol), max_iters=int(max_iters), check_every=int(check_every),
             newton_tol=1e-11, newton_max_iters=25, damping=0.5, max_halvings=8,
-            nu0=1.0, k1=0.0, k2=0.0, k3=1.0, dt_merge_rtol=0.0)
+            nu0=1.0, k1=0.0, k2=0.0, k3=1.0, dt_merge_rtol=0.0, strips=1)
         _lib.check(self.ctx, self.lib.pg_set_options(self.ctx, ctypes.byref(self.opts)),
                    "pg_set_options")
         self._weights = [torch.as_tensor(g.weights, device=self.device) for g in self.grids]

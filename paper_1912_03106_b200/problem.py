@@ -91,7 +91,8 @@ class GpuFemProblem:
             max_halvings=int(nt.get("max_halvings", 8)),
             nu0=float(spec["nu0"]), k1=float(nl.get("k1", 0.0)),
             k2=float(nl.get("k2", 0.0)), k3=float(nl.get("k3", 1.0)),
-            dt_merge_rtol=float(inner_spec.get("dt_merge_rtol", 0.0)))
+            dt_merge_rtol=float(inner_spec.get("dt_merge_rtol", 0.0)),
+            strips=int(bool(inner_spec.get("strips", True))))
         _lib.check(self.ctx, self.lib.pg_set_options(self.ctx, ctypes.byref(self.opts)),
                    "pg_set_options")
         self._weights = [torch.as_tensor(g.weights, device=self.device) for g in self.grids]
@@ -131,6 +132,14 @@ class GpuFemProblem:
         idx = self.lib.pg_add_level(self.ctx, ctypes.byref(d))
         if idx < 0:
             _lib.check(self.ctx, _lib.PG_EINVAL, "pg_add_level")
+
+    def use_strips(self, on=True):
+        """Switch the banded-Cholesky Phi of large grids between the strip
+        solve (default) and the natural-order band solve (the reference's
+        dpbtrs ordering); both are exact direct solves."""
+        self.opts.strips = int(bool(on))
+        _lib.check(self.ctx, self.lib.pg_set_options(self.ctx, ctypes.byref(self.opts)),
+                   "pg_set_options")
 
     def close(self):
         if getattr(self, "ctx", None):

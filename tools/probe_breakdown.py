@@ -64,3 +64,5 @@ print(json.dumps({"wall_s": wall, "iterations": run.iterations, "phi_ms": tot,
 for k in sorted(agg, key=lambda k: -agg[k][1]):
     n, ms = agg[k]
     print(f"grid {k[0]} B={k[1]:5d}: {n:5d} calls, {ms:8.1f} ms, {ms / n * 1e3:7.0f} us/call")
+free, total = torch.cuda.mem_get_info()
+print(f"GPU memory in use {(total - free) / 1e9:.1f} GB of {total / 1e9:.1f} GB")
