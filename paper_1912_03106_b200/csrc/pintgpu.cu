@@ -1706,7 +1706,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
 
 // factor of the strip system and S^-1 = (A^-1)_pp for factor f of the level:
 // the separator unit vectors are solved with the level's own natural-order
-// banded factor, 512 columns at a time
+// banded factor, 1,024 columns at a time
 static int strips_factor(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
     Level::Strips& T = L.strips;
     Level& Sy = *T.sys;
@@ -1720,7 +1720,10 @@ static int strips_factor(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
     const size_t sbytes = (size_t)g.ldp * g.ldp * sizeof(double);
     CU(cudaMalloc(&T.Sinv[sf], sbytes));
     CU(cudaMemsetAsync(T.Sinv[sf], 0, sbytes, st));
-    const int CH = 512;
+    // 1,024 columns per batch: plain chains (a SPIKE-partitioned batch would
+    // first build the 1 GB-per-direction chunk responses of a factor that the
+    // solves themselves never partition)
+    const int CH = 1024;
     double *E = nullptr, *X = nullptr, *dc = nullptr;
     struct Tmp {
         double *&a, *&b, *&c;
