@@ -72,8 +72,10 @@ struct Level {
         std::vector<int4> hch;            // host copy of the chunks
         // strip solves: the same column groups with the strip system's factor
         // ids, and the <= 64-column tiles of the separator GEMM
-        int4* schunks = nullptr; int4* stiles = nullptr; int n_stiles = 0;
-        int4* wchunks = nullptr; int n_wch = 0;      // <= 128-column groups (k_band_wcol)
+        struct StripLists {
+            int4* schunks = nullptr; int4* stiles = nullptr; int n_stiles = 0;
+            int4* wchunks = nullptr; int n_wch = 0;  // column groups of one k_band_wcol CTA
+        } sl[2];                                      // per strip configuration
     };
     std::unordered_map<uint64_t, std::vector<Group>> groups;
     Group tmp_group{};
@@ -117,7 +119,9 @@ struct Level {
         int sinv_cap = 0;
         double *Y1 = nullptr, *Gp = nullptr, *Xp = nullptr;   // one strip-ordered buffer
         int cap_B = 0;
-    } strips;
+        int which = 0;                      // 0: 8 strips, batches that fill the GPU with
+                                            // 128-column CTAs; 1: 16 strips, smaller batches
+    } strips[2];
     int* d_status = nullptr;
     // nonlinear iron elements
     int n_elem = 0;
@@ -359,9 +363,11 @@ static void free_level(Level& L) {
         for (auto& gr : kv.second) {
             cudaFree(gr.perm);
             cudaFree(gr.chunks);
-            if (gr.schunks) cudaFree(gr.schunks);
-            if (gr.stiles) cudaFree(gr.stiles);
-            if (gr.wchunks) cudaFree(gr.wchunks);
+            for (auto& q : gr.sl) {
+                if (q.schunks) cudaFree(q.schunks);
+                if (q.stiles) cudaFree(q.stiles);
+                if (q.wchunks) cudaFree(q.wchunks);
+            }
         }
     L.groups.clear();
     double* nk[] = {L.nk_u, L.nk_F, L.nk_D, L.nk_rhs, L.nk_R, L.nk_Z, L.nk_P, L.nk_Q,
@@ -371,14 +377,16 @@ static void free_level(Level& L) {
     if (L.nk_act) cudaFree(L.nk_act);
     if (L.nk_flag) cudaFree(L.nk_flag);
     if (L.kj) cudaFree(L.kj);
-    if (L.strips.sys) {
-        free_level(*L.strips.sys);
-        delete L.strips.sys;
-        L.strips.sys = nullptr;
+    for (auto& T : L.strips) {
+        if (T.sys) {
+            free_level(*T.sys);
+            delete T.sys;
+            T.sys = nullptr;
+        }
+        for (double* p : T.Sinv) if (p) cudaFree(p);
+        void* sp[] = {T.d_Sinv, T.Y1, T.Gp, T.Xp};
+        for (void* p : sp) if (p) cudaFree(p);
     }
-    for (double* p : L.strips.Sinv) if (p) cudaFree(p);
-    void* sp[] = {L.strips.d_Sinv, L.strips.Y1, L.strips.Gp, L.strips.Xp};
-    for (void* p : sp) if (p) cudaFree(p);
 }
 
 extern "C" void pg_destroy(pg_ctx* ctx) {
@@ -601,9 +609,9 @@ static int build_level(pg_ctx* ctx, const pg_level_desc* d, Level& L) {
 // side = 8 (h + 1) - 1 (the nested grids 2^k - 1), h >= 7.  Builds the
 // permuted block-diagonal operator A_ss (strips padded to whole 32-row blocks
 // with identity rows) as a second, hidden banded level.
-static int build_strips(pg_ctx* ctx, const pg_level_desc* d, Level& L) {
+static int build_strips(pg_ctx* ctx, const pg_level_desc* d, Level& L, int which) {
     static const int on = []{ const char* e = getenv("PG_STRIPS"); return e && e[0] ? atoi(e) : 1; }();
-    const int side = d->side, S = 8;
+    const int side = d->side, S = which == 0 ? 8 : 16;
     // (127^2 and below: the natural-order chains are faster, 3.2 vs 4.5 ms per
     // 4,096 columns -- the gather / scatter passes and the dense separator GEMM
     // outweigh the saved chain work)
@@ -611,6 +619,10 @@ static int build_strips(pg_ctx* ctx, const pg_level_desc* d, Level& L) {
     if (!on || d->n_elem > 0 || side < min_side || side < 63 || (long long)side * side != d->n ||
         (side + 1) % S)
         return 0;
+    // 16 strips (twice the separator unknowns, half the chain length): the
+    // batches too small for 128-column CTAs on the largest grids
+    static const int small_on = []{ const char* e = getenv("PG_STRIPS_SMALL"); return e && e[0] ? atoi(e) : 1; }();
+    if (which == 1 && (!small_on || side < 511)) return 0;
     const int h = (side + 1) / S - 1;
     if (L.bw < side || !L.band_ok) return 0;           // not a natural-order grid stencil
     StripGeo g{};
@@ -661,8 +673,9 @@ static int build_strips(pg_ctx* ctx, const pg_level_desc* d, Level& L) {
         delete sys;
         return 0;                                       // no strips: the natural band solve stays
     }
-    L.strips.geo = g;
-    L.strips.sys = sys;
+    L.strips[which].geo = g;
+    L.strips[which].sys = sys;
+    L.strips[which].which = which;
     return 0;
 }
 
@@ -675,7 +688,7 @@ extern "C" int pg_add_level(pg_ctx* ctx, const pg_level_desc* d) {
     CU(cudaSetDevice(ctx->device));
     Level L;
     if (build_level(ctx, d, L) != 0) { free_level(L); return -1; }
-    if (build_strips(ctx, d, L) != 0) { free_level(L); return -1; }
+    if (build_strips(ctx, d, L, 0) != 0 || build_strips(ctx, d, L, 1) != 0) { free_level(L); return -1; }
     ctx->levels.push_back(L);
     return (int)ctx->levels.size() - 1;
 }
@@ -1707,8 +1720,7 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
 // factor of the strip system and S^-1 = (A^-1)_pp for factor f of the level:
 // the separator unit vectors are solved with the level's own natural-order
 // banded factor, 1,024 columns at a time
-static int strips_factor(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
-    Level::Strips& T = L.strips;
+static int strips_factor(pg_ctx* ctx, Level& L, Level::Strips& T, int f, cudaStream_t st) {
     Level& Sy = *T.sys;
     if ((int)T.fmap.size() <= f) T.fmap.resize(L.FL.size(), -1);
     if (T.fmap[f] >= 0) return PG_OK;
@@ -1758,10 +1770,9 @@ static int strips_factor(pg_ctx* ctx, Level& L, int f, cudaStream_t st) {
     return PG_OK;
 }
 
-static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const double* inv_dt,
-                     const double* inv_dt_host, const double* src, double* u_out,
-                     const double* g, const int* g_idx, cudaStream_t st) {
-    Level::Strips& T = L.strips;
+static int strip_phi(pg_ctx* ctx, Level& L, Level::Strips& T, int B, const double* u_prev,
+                     const double* inv_dt, const double* inv_dt_host, const double* src,
+                     double* u_out, const double* g, const int* g_idx, cudaStream_t st) {
     Level& Sy = *T.sys;
     const StripGeo& geo = T.geo;
     int rc;
@@ -1771,11 +1782,12 @@ static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
                        nullptr, nullptr, &grp)))
         return rc;
     const int BC = grp->BC;
-    if (!grp->schunks) {
+    const int WCOLS = T.which == 0 ? 128 : 32;          // columns of one k_band_wcol CTA
+    if (!grp->sl[T.which].schunks) {
         // the same column groups with the strip system's factor ids, and the
         // <= 64-column tiles of the separator GEMM (per factor)
         for (const int4& q : grp->hch)
-            if ((rc = strips_factor(ctx, L, q.x, st))) return rc;
+            if ((rc = strips_factor(ctx, L, T, q.x, st))) return rc;
         // (the separator solves above went through L.Y: form the rhs again)
         if ((rc = band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st,
                            nullptr, nullptr, nullptr, &grp)))
@@ -1788,19 +1800,21 @@ static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
             const int c0 = sch[i].y, nc = sch[j - 1].y + sch[j - 1].z - c0;
             for (int c = 0; c < nc; c += SG_TN)
                 tiles.push_back(make_int4(sch[i].x, c0 + c, std::min(SG_TN, nc - c), 0));
-            for (int c = 0; c < nc; c += 128)
-                wch.push_back(make_int4(sch[i].x, c0 + c, std::min(128, nc - c), 0));
+            for (int c = 0; c < nc; c += WCOLS)
+                wch.push_back(make_int4(sch[i].x, c0 + c, std::min(WCOLS, nc - c), 0));
             i = j;
         }
-        CU(cudaMalloc(&grp->wchunks, wch.size() * sizeof(int4)));
-        CU(cudaMemcpy(grp->wchunks, wch.data(), wch.size() * sizeof(int4), cudaMemcpyHostToDevice));
-        grp->n_wch = (int)wch.size();
-        CU(cudaMalloc(&grp->schunks, sch.size() * sizeof(int4)));
-        CU(cudaMalloc(&grp->stiles, tiles.size() * sizeof(int4)));
-        CU(cudaMemcpy(grp->schunks, sch.data(), sch.size() * sizeof(int4), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(grp->stiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
-        grp->n_stiles = (int)tiles.size();
+        Level::Group::StripLists& nl = grp->sl[T.which];
+        CU(cudaMalloc(&nl.wchunks, wch.size() * sizeof(int4)));
+        CU(cudaMemcpy(nl.wchunks, wch.data(), wch.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        nl.n_wch = (int)wch.size();
+        CU(cudaMalloc(&nl.stiles, tiles.size() * sizeof(int4)));
+        CU(cudaMemcpy(nl.stiles, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        nl.n_stiles = (int)tiles.size();
+        CU(cudaMalloc(&nl.schunks, sch.size() * sizeof(int4)));
+        CU(cudaMemcpy(nl.schunks, sch.data(), sch.size() * sizeof(int4), cudaMemcpyHostToDevice));
     }
+    const Level::Group::StripLists& SL = grp->sl[T.which];
     if (B > T.cap_B) {
         void* old[] = {T.Y1, T.Gp, T.Xp};
         for (void* p : old) if (p) cudaFree(p);
@@ -1820,35 +1834,40 @@ static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
     const size_t sm = band_solve_smem(Sy, BC);
     static const int wcol = env_flag("PG_STRIP_WCOL", 1);      // 0: k_band_rb chains (A/B)
     auto solve = [&](double* Y) -> int {
-        BandSolveArgs sa{Sy.np, Sy.bwin, Sy.LDA, Sy.nblk, Sy.np, 0, Y, grp->schunks, Sy.d_FL,
+        BandSolveArgs sa{Sy.np, Sy.bwin, Sy.LDA, Sy.nblk, Sy.np, 0, Y, SL.schunks, Sy.d_FL,
                          Sy.nblk, 1, 0, 0, {}};
         for (int dir = 0; dir < 2; ++dir) {
             const bool fwd = dir == 0;
             sa.F = fwd ? Sy.d_FL : Sy.d_FU;
-            const int pk = fwd ? PG_PROF_FWD_W : PG_PROF_BWD_W;
+            const int pk = T.which == 0 ? (fwd ? PG_PROF_FWD_W : PG_PROF_BWD_W)
+                                        : (fwd ? PG_PROF_FWD : PG_PROF_BWD);
             int r;
             if ((r = prof_mark(ctx, pk, st))) return r;
             if (wcol && (Sy.bwin == 64 || Sy.bwin == 32)) {
                 // one CTA per (128-column group, strip): the strips are the
                 // chunks of an exact partition (no coupling across them)
-                sa.chunks = grp->wchunks;
+                sa.chunks = SL.wchunks;
                 sa.q = geo.rows / BD_NB;
                 sa.P = geo.S;
-                dim3 grid(grp->n_wch, geo.S);
-#define PG_WCOL(CW_, FWD_)                                                                  \
+                dim3 grid(SL.n_wch, geo.S);
+#define PG_WCOL(CW_, FWD_, NWC_, NCW_)                                                      \
     do {                                                                                    \
-        constexpr size_t wsm = wcol_smem_bytes<CW_, 1, 8, 16, 4>();                         \
-        SMEM_ATTR_ONCE((k_band_wcol<CW_, 1, FWD_, 8, 16, 4>), wsm);                         \
-        k_band_wcol<CW_, 1, FWD_, 8, 16, 4><<<grid, 288, wsm, st>>>(sa);                    \
+        constexpr size_t wsm = wcol_smem_bytes<CW_, 1, NWC_, NCW_, 4>();                    \
+        SMEM_ATTR_ONCE((k_band_wcol<CW_, 1, FWD_, NWC_, NCW_, 4>), wsm);                    \
+        k_band_wcol<CW_, 1, FWD_, NWC_, NCW_, 4><<<grid, 32 * (NWC_ + 1), wsm, st>>>(sa);   \
     } while (0)
-                if (Sy.bwin == 64) {
-                    if (fwd) PG_WCOL(64, true); else PG_WCOL(64, false);
+                if (T.which == 1) {
+                    // small batches: 4 warps x 8 columns per CTA
+                    if (Sy.bwin == 64) { if (fwd) PG_WCOL(64, true, 4, 8); else PG_WCOL(64, false, 4, 8); }
+                    else { if (fwd) PG_WCOL(32, true, 4, 8); else PG_WCOL(32, false, 4, 8); }
+                } else if (Sy.bwin == 64) {
+                    if (fwd) PG_WCOL(64, true, 8, 16); else PG_WCOL(64, false, 8, 16);
                 } else {
-                    if (fwd) PG_WCOL(32, true); else PG_WCOL(32, false);
+                    if (fwd) PG_WCOL(32, true, 8, 16); else PG_WCOL(32, false, 8, 16);
                 }
 #undef PG_WCOL
                 LAUNCHED();
-                sa.chunks = grp->schunks;
+                sa.chunks = SL.schunks;
                 sa.q = Sy.nblk;
                 sa.P = 1;
             } else if ((r = band_dir(ctx, Sy, BC, fwd, sa, dim3(grp->nch, 1), sm, st))) {
@@ -1865,8 +1884,8 @@ static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
         geo, B, L.row_ptr, L.col_idx, L.m_val, L.k_val, inv_dt, grp->perm, L.Y, T.Y1, T.Gp);
     LAUNCHED();
     SMEM_ATTR_ONCE(k_strip_sinv_gemm, SG_SMEM);
-    k_strip_sinv_gemm<<<dim3(geo.ldp / SG_TM, 1, grp->n_stiles), 256, SG_SMEM, st>>>(
-        geo.ldp, T.d_Sinv, T.Gp, T.Xp, grp->stiles);
+    k_strip_sinv_gemm<<<dim3(geo.ldp / SG_TM, 1, SL.n_stiles), 256, SG_SMEM, st>>>(
+        geo.ldp, T.d_Sinv, T.Gp, T.Xp, SL.stiles);
     LAUNCHED();
     if ((rc = prof_mark(ctx, PG_PROF_FIX, st))) return rc;
     // second solve on b_s - A_sp x_p: the strip buffer is re-gathered from the
@@ -1896,7 +1915,7 @@ static int strip_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const d
         for (const int4& q : grp->hch) used[T.fmap[q.x]] = 1;
         double fb = 0.0;
         for (char u : used) fb += u ? bd_block_doubles(Sy.bwin) * Sy.nblk * 8.0 : 0.0;
-        for (int k : {PG_PROF_FWD_W, PG_PROF_BWD_W}) {
+        for (int k : {T.which == 0 ? PG_PROF_FWD_W : PG_PROF_FWD, T.which == 0 ? PG_PROF_BWD_W : PG_PROF_BWD}) {
             ctx->prof_flops[k] += 2.0 * (2.0 * geo.n_ss * (double)Sy.bw * Bd);
             ctx->prof_bytes[k] += 2.0 * (16.0 * geo.n_ss * Bd + fb);
         }
@@ -1997,9 +2016,16 @@ extern "C" int pg_phi_batch_h(pg_ctx* ctx, int level, int B, const double* u_pre
         // (PG_STRIPS_MIN_B / PG_STRIPS_MIN_SIDE: test overrides -- the parity
         // tests push the strip solve through the small reference fixtures)
         static const int strips_min_b = env_flag("PG_STRIPS_MIN_B", 0);
-        if (L.strips.sys && ctx->opts.strips && band_rb_on() &&
-            B >= (strips_min_b > 0 ? strips_min_b : 26 * ctx->n_sm))
-            return strip_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
+        const int big = strips_min_b > 0 ? strips_min_b : 26 * ctx->n_sm;
+        if (ctx->opts.strips && band_rb_on()) {
+            if (L.strips[0].sys && B >= big)
+                return strip_phi(ctx, L, L.strips[0], B, u_prev, inv_dt, inv_dt_host, src, u_out, g,
+                                 g_idx, st);
+            // smaller batches of the largest grids: 16 strips, 32-column CTAs
+            if (L.strips[1].sys && B >= 8 && B < big)
+                return strip_phi(ctx, L, L.strips[1], B, u_prev, inv_dt, inv_dt_host, src, u_out, g,
+                                 g_idx, st);
+        }
         return band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st);
     } else if (L.resident) {
         if ((rc = launch_resident(ctx, L, B, u_prev, guess, inv_dt, src, u_out, g, g_idx, st)))
