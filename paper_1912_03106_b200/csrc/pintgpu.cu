@@ -1786,6 +1786,20 @@ static int strip_phi(pg_ctx* ctx, Level& L, Level::Strips& T, int B, const doubl
     if (!grp->sl[T.which].schunks) {
         // the same column groups with the strip system's factor ids, and the
         // <= 64-column tiles of the separator GEMM (per factor)
+        {
+            // factor the strip systems of every new 1/dt of the group in ONE
+            // launch (one CTA per factor) before the per-factor separator setups
+            if (T.fmap.size() < L.FL.size()) T.fmap.resize(L.FL.size(), -1);
+            std::vector<double> cs;
+            for (const int4& q : grp->hch)
+                if (T.fmap[q.x] < 0 &&
+                    std::find(cs.begin(), cs.end(), L.fac_c[q.x]) == cs.end())
+                    cs.push_back(L.fac_c[q.x]);
+            if (!cs.empty()) {
+                std::vector<int> ids(cs.size());
+                if ((rc = factor_ids(ctx, Sy, cs.data(), (int)cs.size(), ids.data(), st))) return rc;
+            }
+        }
         for (const int4& q : grp->hch)
             if ((rc = strips_factor(ctx, L, T, q.x, st))) return rc;
         // (the separator solves above went through L.Y: form the rhs again)
