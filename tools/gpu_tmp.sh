@@ -1,2 +1,7 @@
 mkdir -p gpurun_out
-PG_DEBUG_SETUP=1 timeout 900 python tools/probe_e2e4.py > gpurun_out/e2e4.txt 2>&1
+rm -f /tmp/strips_*.npy
+for B in 256 4096; do
+( PG_STRIPS=0 timeout 900 python tools/probe_strips.py 512 $B; PG_STRIPS=1 timeout 900 python tools/probe_strips.py 512 $B; PG_STRIP_NATB=0 timeout 900 python tools/probe_strips.py 512 $B ) > gpurun_out/strips_natb_512_B$B.txt 2>&1
+rm -f /tmp/strips_*.npy
+done
+timeout 900 python -m pytest tests/test_gpu_strips.py -q > gpurun_out/pytest_strips.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strips.log
