@@ -1541,9 +1541,13 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             if (B > L.perm_cap) {
                 if (L.d_perm) cudaFree(L.d_perm);
                 if (L.d_chunks) cudaFree(L.d_chunks);
-                L.perm_cap = std::max(B, 64);
-                CU(cudaMalloc(&L.d_perm, L.perm_cap * sizeof(int)));
-                CU(cudaMalloc(&L.d_chunks, L.perm_cap * sizeof(int4)));
+                L.d_perm = nullptr;
+                L.d_chunks = nullptr;
+                L.perm_cap = 0;
+                const int cap = std::max(B, 64);
+                CU(cudaMalloc(&L.d_perm, cap * sizeof(int)));
+                CU(cudaMalloc(&L.d_chunks, cap * sizeof(int4)));
+                L.perm_cap = cap;
             }
             if ((rc = pin_upload(ctx, L.d_perm, perm.data(), B * sizeof(int), st))) return rc;
             if ((rc = pin_upload(ctx, L.d_chunks, chunks.data(), chunks.size() * sizeof(int4), st)))
@@ -1568,8 +1572,10 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     const int nch = grp->nch;
     if (B > L.Y_B) {
         if (L.Y) cudaFree(L.Y);
-        L.Y_B = B;
+        L.Y = nullptr;
+        L.Y_B = 0;                       // (stays 0 if the allocation fails: a retry re-allocates)
         CU(cudaMalloc(&L.Y, (size_t)B * L.np * sizeof(double)));
+        L.Y_B = B;
     }
     dim3 gr((L.np + 255) / 256, (B + BD_RHS_CB - 1) / BD_RHS_CB);
     // the scatter (unpartitioned chains) is fused into the k-split backward chain
@@ -1639,8 +1645,10 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
         const size_t tneed = (size_t)P * L.bwin * B;
         if (tneed > L.spk_T_cap) {
             if (L.spk_T) cudaFree(L.spk_T);
-            L.spk_T_cap = tneed;
+            L.spk_T = nullptr;
+            L.spk_T_cap = 0;
             CU(cudaMalloc(&L.spk_T, tneed * sizeof(double)));
+            L.spk_T_cap = tneed;
         }
     }
     BandSolveArgs sa{L.np, L.bwin, L.LDA, L.nblk, L.np, 0, L.Y, d_chunks, L.d_FL,
@@ -1730,7 +1738,7 @@ static int strips_factor(pg_ctx* ctx, Level& L, Level::Strips& T, int f, cudaStr
     if ((int)T.Sinv.size() <= sf) T.Sinv.resize(sf + 1, nullptr);
     const StripGeo& g = T.geo;
     const size_t sbytes = (size_t)g.ldp * g.ldp * sizeof(double);
-    CU(cudaMalloc(&T.Sinv[sf], sbytes));
+    if (!T.Sinv[sf]) CU(cudaMalloc(&T.Sinv[sf], sbytes));
     CU(cudaMemsetAsync(T.Sinv[sf], 0, sbytes, st));
     // 1,024 columns per batch: plain chains (a SPIKE-partitioned batch would
     // first build the 1 GB-per-direction chunk responses of a factor that the
@@ -1833,10 +1841,11 @@ static int strip_phi(pg_ctx* ctx, Level& L, Level::Strips& T, int B, const doubl
         void* old[] = {T.Y1, T.Gp, T.Xp};
         for (void* p : old) if (p) cudaFree(p);
         T.Y1 = T.Gp = T.Xp = nullptr;
-        T.cap_B = B;
+        T.cap_B = 0;
         CU(cudaMalloc(&T.Y1, (size_t)B * geo.n_ss * sizeof(double)));
         CU(cudaMalloc(&T.Gp, (size_t)B * geo.ldp * sizeof(double)));
         CU(cudaMalloc(&T.Xp, (size_t)B * geo.ldp * sizeof(double)));
+        T.cap_B = B;
     }
     const int xt = (geo.side + 31) / 32;
     const size_t tsm = (size_t)geo.h * 33 * sizeof(double);

@@ -218,10 +218,18 @@ class GpuFemProblem:
         hp = None
         if inv_dt_host is not None:
             hp = inv_dt_host.ctypes.data_as(ctypes.c_void_p)
-        rc = self.lib.pg_phi_batch_h(self.ctx, int(level), B, _lib.ptr(u_prev),
-                                     _lib.ptr(guess), _lib.ptr(inv_dt), hp,
-                                     _lib.ptr(src) if self.n_src else None, _lib.ptr(out),
-                                     _lib.ptr(g), _lib.ptr(g_idx), self._stream())
+        def call():
+            return self.lib.pg_phi_batch_h(self.ctx, int(level), B, _lib.ptr(u_prev),
+                                           _lib.ptr(guess), _lib.ptr(inv_dt), hp,
+                                           _lib.ptr(src) if self.n_src else None, _lib.ptr(out),
+                                           _lib.ptr(g), _lib.ptr(g_idx), self._stream())
+        rc = call()
+        if rc == _lib.PG_ECUDA and b"out of memory" in (self.lib.pg_last_error(self.ctx) or b""):
+            # the library allocates its workspaces with cudaMalloc: hand it the
+            # blocks torch's caching allocator holds but does not use, once
+            torch.cuda.synchronize(self.device)
+            torch.cuda.empty_cache()
+            rc = call()
         if rc == _lib.PG_ENEWTON:
             col, its = ctypes.c_int(), ctypes.c_int()
             self.lib.pg_newton_failure(self.ctx, ctypes.byref(col), ctypes.byref(its))
