@@ -1361,7 +1361,9 @@ template <int UU, int NS, int MINB, int CC>
 __global__ void __launch_bounds__(256, MINB)
 k_band_rhs_dia_t(RhsDia a, const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
                  const double* __restrict__ src, const int* __restrict__ perm,
-                 double* __restrict__ Y) {
+                 double* __restrict__ Y, double* __restrict__ uo) {
+    // uo != NULL: column gc goes to uo[perm[gc]][0..n) (the caller's output
+    // array used as scratch for the right-hand sides) instead of Y[gc][0..ldy)
     __shared__ int sp[CC];
     __shared__ double sc[CC], ss[CC][NS];
     const int gc0 = blockIdx.y * CC;
@@ -1379,7 +1381,8 @@ k_band_rhs_dia_t(RhsDia a, const double* __restrict__ u_prev, const double* __re
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.ldy) return;
     if (i >= a.n) {
-        for (int j = 0; j < ncol; ++j) Y[(size_t)(gc0 + j) * a.ldy + i] = 0.0;
+        if (!uo)
+            for (int j = 0; j < ncol; ++j) Y[(size_t)(gc0 + j) * a.ldy + i] = 0.0;
         return;
     }
     double mup[UU], mlo[UU];
@@ -1414,7 +1417,9 @@ k_band_rhs_dia_t(RhsDia a, const double* __restrict__ u_prev, const double* __re
 #pragma unroll
             for (int q = 0; q < NS; ++q) f = fma(ss[j][q], sh[q], f);
         }
-        yo[(size_t)j * a.ldy] = fma(sc[j], v, f);
+        const double bv = fma(sc[j], v, f);
+        if (uo) uo[(size_t)sp[j] * a.n + i] = bv;
+        else yo[(size_t)j * a.ldy] = bv;
     }
 }
 

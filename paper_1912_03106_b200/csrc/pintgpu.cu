@@ -1483,7 +1483,11 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
                     const double* inv_dt_host, const double* src, double* u_out,
                     const double* g, const int* g_idx, cudaStream_t st,
                     const double* copy_src = nullptr, const int* sub = nullptr,
-                    const int* fid_all = nullptr, Level::Group** rhs_only = nullptr) {
+                    const int* fid_all = nullptr, Level::Group** rhs_only = nullptr,
+                    bool* rhs_in_uout = nullptr) {
+    // rhs_in_uout (with rhs_only): the caller's u_out may serve as scratch for
+    // the right-hand sides (column b at u_out[b]) instead of L.Y, when the rhs
+    // kernel in use supports it; *rhs_in_uout reports whether it did
     // rhs_only: stop after the right-hand sides are in L.Y (natural rows,
     // grouped columns) and hand the column grouping back (strip solves)
     // fid_all (preconditioner mode): factor of every full-batch column, chosen
@@ -1570,7 +1574,12 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
     const int* d_perm = grp->perm;
     const int4* d_chunks = grp->chunks;
     const int nch = grp->nch;
-    if (B > L.Y_B) {
+    const int ldh_rhs = (256 + 2 * L.omax + 255) / 256;
+    const bool to_uout = rhs_only && rhs_in_uout && L.dia && !copy_src && L.U == 3 &&
+                         L.n_src <= 4 && ldh_rhs > 4 && env_flag("PG_RHS_DIA", 1) &&
+                         env_flag("PG_RHS_T", 1) && env_flag("PG_RHS_SM", 2) != 3;
+    if (rhs_in_uout) *rhs_in_uout = to_uout;
+    if (!to_uout && B > L.Y_B) {
         if (L.Y) cudaFree(L.Y);
         L.Y = nullptr;
         L.Y_B = 0;                       // (stays 0 if the allocation fails: a retry re-allocates)
@@ -1614,8 +1623,8 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             // columns per CTA measured slower).  PG_RHS_T=0: generic (A/B)
             static const int rhs_t = env_flag("PG_RHS_T", 1);
             if (L.U == 3 && L.n_src <= 4 && rhs_t)
-                k_band_rhs_dia_t<3, 4, 5, BD_RHS_CC><<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src,
-                                                                          d_perm, L.Y);
+                k_band_rhs_dia_t<3, 4, 5, BD_RHS_CC><<<grd, 256, 0, st>>>(
+                    ra, u_prev, inv_dt, src, d_perm, L.Y, to_uout ? u_out : nullptr);
             else
                 k_band_rhs_dia<<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y);
         }
@@ -1785,9 +1794,12 @@ static int strip_phi(pg_ctx* ctx, Level& L, Level::Strips& T, int B, const doubl
     const StripGeo& geo = T.geo;
     int rc;
     // right-hand sides in natural order (grouped columns) + the grouping
+    // (they go into u_out itself -- scratch until the final scatter -- where the
+    // rhs kernel supports it: no [B][n] workspace besides the strip buffer)
     Level::Group* grp = nullptr;
+    bool in_uout = false;
     if ((rc = band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st, nullptr,
-                       nullptr, nullptr, &grp)))
+                       nullptr, nullptr, &grp, &in_uout)))
         return rc;
     const int BC = grp->BC;
     const int WCOLS = T.which == 0 ? 128 : 32;          // columns of one k_band_wcol CTA
@@ -1812,7 +1824,7 @@ static int strip_phi(pg_ctx* ctx, Level& L, Level::Strips& T, int B, const doubl
             if ((rc = strips_factor(ctx, L, T, q.x, st))) return rc;
         // (the separator solves above went through L.Y: form the rhs again)
         if ((rc = band_phi(ctx, L, B, u_prev, inv_dt, inv_dt_host, src, u_out, g, g_idx, st,
-                           nullptr, nullptr, nullptr, &grp)))
+                           nullptr, nullptr, nullptr, &grp, &in_uout)))
             return rc;
         std::vector<int4> sch(grp->hch), tiles, wch;
         for (int4& q : sch) q.x = T.fmap[q.x];
@@ -1847,10 +1859,11 @@ static int strip_phi(pg_ctx* ctx, Level& L, Level::Strips& T, int B, const doubl
         CU(cudaMalloc(&T.Xp, (size_t)B * geo.ldp * sizeof(double)));
         T.cap_B = B;
     }
+    const double* Yn = in_uout ? u_out : L.Y;           // natural-order right-hand sides
     const int xt = (geo.side + 31) / 32;
     const size_t tsm = (size_t)geo.h * 33 * sizeof(double);
     if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
-    k_strip_gather<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, L.Y, T.Y1, nullptr);
+    k_strip_gather<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, Yn, in_uout ? grp->perm : nullptr, T.Y1, nullptr);
     LAUNCHED();
     if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
     // chains of the strip system: window h + 1, unpartitioned, no fused scatter
@@ -1904,7 +1917,8 @@ static int strip_phi(pg_ctx* ctx, Level& L, Level::Strips& T, int B, const doubl
     const int gy = std::min(B, 16384);
     if ((rc = prof_mark(ctx, PG_PROF_FIX, st))) return rc;
     k_strip_g<<<dim3((geo.ldp + 255) / 256, gy), 256, 0, st>>>(
-        geo, B, L.row_ptr, L.col_idx, L.m_val, L.k_val, inv_dt, grp->perm, L.Y, T.Y1, T.Gp);
+        geo, B, L.row_ptr, L.col_idx, L.m_val, L.k_val, inv_dt, grp->perm, Yn, in_uout ? 1 : 0, T.Y1,
+        T.Gp);
     LAUNCHED();
     SMEM_ATTR_ONCE(k_strip_sinv_gemm, SG_SMEM);
     k_strip_sinv_gemm<<<dim3(geo.ldp / SG_TM, 1, SL.n_stiles), 256, SG_SMEM, st>>>(
@@ -1915,7 +1929,7 @@ static int strip_phi(pg_ctx* ctx, Level& L, Level::Strips& T, int B, const doubl
     // natural right-hand sides (one strip-ordered buffer instead of two: 8.4 GB
     // at 511^2 x 4,096 columns)
     if ((rc = prof_mark(ctx, PG_PROF_SCATTER, st))) return rc;
-    k_strip_gather<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, L.Y, T.Y1, nullptr);
+    k_strip_gather<<<dim3(xt * geo.S, B), 256, tsm, st>>>(geo, Yn, in_uout ? grp->perm : nullptr, T.Y1, nullptr);
     LAUNCHED();
     k_strip_update<<<dim3((2 * (geo.S - 1) * geo.side + 255) / 256, gy), 256, 0, st>>>(
         geo, B, L.row_ptr, L.col_idx, L.m_val, L.k_val, inv_dt, grp->perm, T.Xp, T.Y1);

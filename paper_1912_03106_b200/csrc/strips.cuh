@@ -48,14 +48,15 @@ __device__ __forceinline__ int nat_to_strip(const StripGeo& g, int i) {
 // 32 h contiguous doubles out, transposed through shared memory.
 // grid (ceil(side / 32) * S, columns), 256 threads; smem h * 33 doubles
 __global__ void __launch_bounds__(256)
-k_strip_gather(StripGeo g, const double* __restrict__ Yn, double* __restrict__ Y1,
-               double* __restrict__ Y2) {
+k_strip_gather(StripGeo g, const double* __restrict__ Yn, const int* __restrict__ nperm,
+               double* __restrict__ Y1, double* __restrict__ Y2) {
+    // nperm != NULL: natural column col lives at Yn[nperm[col]][0..n) (stride n)
     extern __shared__ double tile[];                  // [h][33]
     const int xt = (g.side + 31) / 32;
     const int s = blockIdx.x / xt, x0 = (blockIdx.x - s * xt) * 32;
     const int nx = min(32, g.side - x0);
     const size_t col = blockIdx.y;
-    const double* yn = Yn + col * g.ldn;
+    const double* yn = nperm ? Yn + (size_t)nperm[col] * g.n : Yn + col * g.ldn;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int yl = ty; yl < g.h; yl += 8)
         if (tx < nx) tile[yl * 33 + tx] = yn[(size_t)(s * (g.h + 1) + yl) * g.side + x0 + tx];
@@ -83,7 +84,9 @@ __global__ void __launch_bounds__(256)
 k_strip_g(StripGeo g, int B, const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
           const double* __restrict__ m_val, const double* __restrict__ k_val,
           const double* __restrict__ inv_dt, const int* __restrict__ perm,
-          const double* __restrict__ Yn, const double* __restrict__ Y1, double* __restrict__ Gp) {
+          const double* __restrict__ Yn, int yn_perm, const double* __restrict__ Y1,
+          double* __restrict__ Gp) {
+    // yn_perm != 0: natural column col lives at Yn[perm[col]][0..n) (stride n)
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= g.ldp) return;
     for (int col = blockIdx.y; col < B; col += gridDim.y) {
@@ -92,7 +95,7 @@ k_strip_g(StripGeo g, int B, const int* __restrict__ row_ptr, const int* __restr
             const int s = j / g.side, x = j - s * g.side;
             const int i = (s * (g.h + 1) + g.h) * g.side + x;
             const double c = inv_dt[perm[col]];
-            v = Yn[(size_t)col * g.ldn + i];
+            v = yn_perm ? Yn[(size_t)perm[col] * g.n + i] : Yn[(size_t)col * g.ldn + i];
             const double* y1 = Y1 + (size_t)col * g.n_ss;
             for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
                 const int r = nat_to_strip(g, col_idx[e]);
