@@ -1752,7 +1752,16 @@ static int strips_factor(pg_ctx* ctx, Level& L, Level::Strips& T, int f, cudaStr
     // 1,024 columns per batch: plain chains (a SPIKE-partitioned batch would
     // first build the 1 GB-per-direction chunk responses of a factor that the
     // solves themselves never partition)
-    const int CH = 1024;
+    int CH = 1024;
+    {
+        // ... fewer when memory is short (two [CH][n] temporaries): at least 128
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const size_t per_col = 2 * (size_t)g.n * sizeof(double) + (size_t)L.np * sizeof(double);
+            const size_t fit = free_b > (size_t)3 << 30 ? (free_b - ((size_t)2 << 30)) / per_col : 0;
+            CH = (int)std::max<size_t>(128, std::min<size_t>(1024, fit / 64 * 64));
+        }
+    }
     double *E = nullptr, *X = nullptr, *dc = nullptr;
     struct Tmp {
         double *&a, *&b, *&c;
