@@ -1754,12 +1754,14 @@ static int strips_factor(pg_ctx* ctx, Level& L, Level::Strips& T, int f, cudaStr
     // solves themselves never partition)
     int CH = 1024;
     {
-        // ... fewer when memory is short (two [CH][n] temporaries): at least 128
+        // ... as many as a third of the free memory holds (two [CH][n]
+        // temporaries + the solve's workspace): wider batches run wider column
+        // groups (4,096 columns: 25 ms per 1,024 against 44 ms), at least 128
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
             const size_t per_col = 2 * (size_t)g.n * sizeof(double) + (size_t)L.np * sizeof(double);
-            const size_t fit = free_b > (size_t)3 << 30 ? (free_b - ((size_t)2 << 30)) / per_col : 0;
-            CH = (int)std::max<size_t>(128, std::min<size_t>(1024, fit / 64 * 64));
+            const size_t fit = free_b / 3 / per_col;
+            CH = (int)std::max<size_t>(128, std::min<size_t>(4096, fit / 64 * 64));
         }
     }
     double *E = nullptr, *X = nullptr, *dc = nullptr;

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-( time timeout 2400 python bench.py --gpus 1 --steps 20 --warmup 5 ) > gpurun_out/bench_driver.log 2> gpurun_out/bench_driver.err; echo "bench rc=$?" >> gpurun_out/bench_driver.err
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 9000 --launch-count 6000 --csv --log-file gpurun_out/launches_bench_r02h.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-phi --no-seq --no-cfg2 --no-cfg3 --no-natural > gpurun_out/ncu_bench.log 2>&1
-echo "ncu bench rc=$?" >> gpurun_out/ncu_bench.log
+timeout 900 python tools/probe_e2e4.py > gpurun_out/e2e4.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_strips.py tests/test_gpu_phi.py -q -k "strip or wide" > gpurun_out/pytest_strips.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strips.log
