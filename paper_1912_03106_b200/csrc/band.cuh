@@ -1357,7 +1357,7 @@ k_band_rhs_dia(RhsDia a, const double* __restrict__ u_prev, const double* __rest
 // the source shapes, so 4 CTAs per SM stay resident (the generic kernel runs 3
 // at 80 registers and is latency-bound at 37 % warps active on the 511^2 grid,
 // profiles/r02c_ncu_rhs_dia_cfg4.json).  Same arithmetic, same order: bit-identical.
-template <int UU, int NS, int MINB, int CC>
+template <int UU, int NS, int MINB, int CC, int UNR = 4>
 __global__ void __launch_bounds__(256, MINB)
 k_band_rhs_dia_t(RhsDia a, const double* __restrict__ u_prev, const double* __restrict__ inv_dt,
                  const double* __restrict__ src, const int* __restrict__ perm,
@@ -1405,7 +1405,7 @@ k_band_rhs_dia_t(RhsDia a, const double* __restrict__ u_prev, const double* __re
         has_src |= sh[q] != 0.0;
     }
     double* yo = Y + (size_t)gc0 * a.ldy + i;
-#pragma unroll 4
+#pragma unroll UNR
     for (int j = 0; j < ncol; ++j) {
         const double* ub = u_prev + (size_t)sp[j] * a.n + i;
         double v = m0 * ub[0];

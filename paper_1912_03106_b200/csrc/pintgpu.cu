@@ -1617,13 +1617,14 @@ static int band_phi(pg_ctx* ctx, Level& L, int B, const double* u_prev, const do
             }
         } else {
             dim3 grd((L.np + 255) / 256, (B + BD_RHS_CC - 1) / BD_RHS_CC);
-            // 7-point stencils with <= 4 sources: the compile-time variant at 5
-            // CTAs per SM (511^2, 4,096 columns: 6.5 ms against 8.3 ms generic and
-            // 9.7 ms for the cp.async ring; 4 / 6 CTAs per SM and 4 / 8 / 16
-            // columns per CTA measured slower).  PG_RHS_T=0: generic (A/B)
+            // 7-point stencils with <= 4 sources: the compile-time variant at 4
+            // CTAs per SM, columns unrolled by 4 (511^2, 4,096 columns: 5.6-6.5 ms
+            // against 8.3 ms generic and 9.7 ms for the cp.async ring; 3 / 5 / 6 / 8
+            // CTAs per SM, unroll 1 / 2 / 3 / 8 and 4 / 8 / 16 columns per CTA
+            // measured within noise or slower).  PG_RHS_T=0: generic (A/B)
             static const int rhs_t = env_flag("PG_RHS_T", 1);
             if (L.U == 3 && L.n_src <= 4 && rhs_t)
-                k_band_rhs_dia_t<3, 4, 5, BD_RHS_CC><<<grd, 256, 0, st>>>(
+                k_band_rhs_dia_t<3, 4, 4, BD_RHS_CC, 4><<<grd, 256, 0, st>>>(
                     ra, u_prev, inv_dt, src, d_perm, L.Y, to_uout ? u_out : nullptr);
             else
                 k_band_rhs_dia<<<grd, 256, 0, st>>>(ra, u_prev, inv_dt, src, d_perm, L.Y);
