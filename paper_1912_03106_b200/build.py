@@ -18,7 +18,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
          "-Xptxas", "-warn-spills"]
 # no library kernels: the CUDA runtime is the only dependency
-LIBS = ["-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+LIBS = ["-Xlinker", "-rpath=/usr/local/cuda/lib64", "-lpthread"]
 
 
 def sources():

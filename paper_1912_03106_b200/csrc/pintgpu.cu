@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -1163,7 +1164,10 @@ static int band_factors(pg_ctx* ctx, Level& L, const std::vector<double>& cs,
     k_band_build<<<gb, 256, 0, st>>>(a, d_c, d_lb, d_kper);
     LAUNCHED();
     const size_t sm = bd_factor_smem(L.bw, bd_cw(L.bwin));
-    CU(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    // (the attribute is per function, and factorisations of different systems
+    // may be in flight from several host threads: always the device maximum)
+    SMEM_ATTR_ONCE(k_band_factor, 232448 - 1024);
+    if (sm > 232448 - 1024) return set_err(ctx, PG_EINVAL, "band too wide to factor (%d)", L.bw);
     k_band_factor<<<nf, 256, sm, st>>>(a, d_lb, L.d_FL + first, L.d_FU + first, L.d_status);
     LAUNCHED();
 
@@ -2008,7 +2012,42 @@ extern "C" int pg_prefactor(pg_ctx* ctx, int level, int n, const double* inv_dt_
     if (L.n_elem > 0 && !L.k_pre) return PG_OK;
     CU(cudaSetDevice(ctx->device));
     std::vector<int> fid(n);
-    return factor_ids(ctx, L, inv_dt_host, n, fid.data(), (cudaStream_t)stream);
+    Level* sys[2] = {nullptr, nullptr};
+    static const int overlap = env_flag("PG_PREFACTOR_STRIPS", 1);
+    // (only where every batch size takes a strip path -- the 16-strip system
+    // exists: grids of 511^2 and more; elsewhere strip factors stay lazy)
+    if (ctx->opts.strips && overlap && L.n_elem == 0 && L.strips[1].sys)
+        for (int k = 0; k < 2; ++k) sys[k] = L.strips[k].sys;
+    if (!sys[0] && !sys[1])
+        return factor_ids(ctx, L, inv_dt_host, n, fid.data(), (cudaStream_t)stream);
+    // The strip systems of the same 1/dt values, factored while the
+    // natural-order factorisation runs: each is one CTA per factor (1.4 s for
+    // the 511^2 natural band, 0.36 s per strip system), so the three launches
+    // share the GPU from three host threads / streams instead of queueing
+    // (the strip factors would otherwise be built lazily inside the first solve).
+    int rcs[3] = {PG_OK, PG_OK, PG_OK};
+    auto work = [&](int k) {
+        if (cudaSetDevice(ctx->device) != cudaSuccess) { rcs[1 + k] = PG_ECUDA; return; }
+        cudaStream_t s2 = nullptr;
+        if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
+            rcs[1 + k] = PG_ECUDA;
+            return;
+        }
+        std::vector<int> ids(n);
+        rcs[1 + k] = factor_ids(ctx, *sys[k], inv_dt_host, n, ids.data(), s2);
+        cudaStreamSynchronize(s2);
+        cudaStreamDestroy(s2);
+    };
+    std::thread th[2];
+    for (int k = 0; k < 2; ++k)
+        if (sys[k]) th[k] = std::thread(work, k);
+    rcs[0] = factor_ids(ctx, L, inv_dt_host, n, fid.data(), (cudaStream_t)stream);
+    for (int k = 0; k < 2; ++k)
+        if (th[k].joinable()) th[k].join();
+    // a strip factorisation that failed here is retried (and reported) by the
+    // first strip solve that needs it
+    if (rcs[0] == PG_OK && (rcs[1] != PG_OK || rcs[2] != PG_OK)) ctx->err.clear();
+    return rcs[0];
 }
 
 extern "C" int pg_phi_batch(pg_ctx* ctx, int level, int B, const double* u_prev,

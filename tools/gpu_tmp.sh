@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-for t in 2 3 4 5 6 7; do PG_STRIPS=0 PG_RHS_T=$t timeout 600 python tools/probe_band.py cfg4 0:4096 2>&1 | tail -1 > gpurun_out/probe_rhs_u$t.txt; done
+PG_DEBUG_SETUP=1 timeout 900 python tools/probe_e2e4.py > gpurun_out/e2e4.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_strips.py tests/test_gpu_phi.py tests/test_gpu_mgrit.py tests/test_gpu_edge.py -q > gpurun_out/pytest_strips.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strips.log
