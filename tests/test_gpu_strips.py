@@ -92,3 +92,30 @@ np.save(sys.argv[1], out.cpu().numpy())
             outs.append(np.load(path))
     rel = np.linalg.norm(outs[0] - outs[1], axis=1) / np.linalg.norm(outs[0], axis=1)
     assert rel.max() < 1e-12, rel.max()
+
+
+def test_use_strips_switches_at_run_time(cuda):
+    """`GpuFemProblem.use_strips` (pg_solver_opts.strips) on a live problem: a
+    GPU-filling batch on the 255^2 grid through the strip solve, then through
+    the natural-order band solve, same inputs -- agreement to rounding."""
+    import torch
+    from paper_1912_03106_b200 import GpuFemProblem, configs
+    spec = configs.config2(N=256, n_steps=2 ** 14, levels=1)
+    prob = GpuFemProblem(spec, inner="cholesky")
+    n, B = prob.spatial.size(0), 3904
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    U = torch.randn(B, n, dtype=torch.float64, device=cuda, generator=gen) * 1e-3
+    dt = 0.02 / 2 ** 14
+    inv_h = np.full(B, 1.0 / dt)
+    inv = torch.as_tensor(inv_h, device=cuda)
+    src = torch.as_tensor(prob.source_values(np.linspace(0.001, 0.019, B)), device=cuda)
+    outs = []
+    for on in (True, False):
+        prob.use_strips(on)
+        out = torch.empty_like(U)
+        prob.phi_batch(0, U, inv, src, out, inv_dt_host=inv_h)
+        outs.append(out)
+    rel = (torch.linalg.vector_norm(outs[0] - outs[1], dim=1)
+           / torch.linalg.vector_norm(outs[1], dim=1)).max().item()
+    assert 0.0 < rel < 1e-12, rel          # two different direct solvers, same answer
+    prob.close()
