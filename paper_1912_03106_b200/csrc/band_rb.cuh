@@ -414,19 +414,24 @@ k_band_wcol(BandSolveArgs a) {
             mbar_wait(&full[buf], (P / NBUF) & 1);
             const double* pc = bufs + (size_t)buf * PIECE;
             if (j == 0) {
+                // D^-1 is lower (D^-T upper) triangular with exact zeros in
+                // the other half: the 8 x 4 operand tiles that lie entirely in
+                // it are skipped at compile time (12 of 32: an eighth of the
+                // step's DMMAs), the result is bit-identical
 #pragma unroll
                 for (int u = 0; u < NB / 4; ++u) {
                     const int kk = 4 * u + q4;
-                    double av[4], bv[NRT];
-#pragma unroll
-                    for (int mi = 0; mi < 4; ++mi) av[mi] = pc[(8 * mi + g) * BD_PD + kk];
+                    double bv[NRT];
 #pragma unroll
                     for (int ni = 0; ni < NRT; ++ni) bv[ni] = bk[(8 * ni + g) * LDR + kk];
 #pragma unroll
-                    for (int mi = 0; mi < 4; ++mi)
+                    for (int mi = 0; mi < 4; ++mi) {
+                        if (FWD ? (u > 2 * mi + 1) : (u < 2 * mi)) continue;
+                        const double av = pc[(8 * mi + g) * BD_PD + kk];
 #pragma unroll
                         for (int ni = 0; ni < NRT; ++ni)
-                            dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+                            dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av, bv[ni]);
+                    }
                 }
             } else {
 #pragma unroll
