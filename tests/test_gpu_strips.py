@@ -119,3 +119,33 @@ def test_use_strips_switches_at_run_time(cuda):
            / torch.linalg.vector_norm(outs[1], dim=1)).max().item()
     assert 0.0 < rel < 1e-12, rel          # two different direct solvers, same answer
     prob.close()
+
+
+def test_engine_on_the_511_grid_strips_vs_natural(cuda):
+    """A short MGRIT solve on the 511^2 grid (64 steps, 2 levels): the engine's
+    setup factors the natural-order system and both strip systems concurrently
+    (pg_prefactor), every Phi call takes a strip path; the same solve with
+    strips off (natural-order chains + SPIKE) gives the same iteration count
+    and residual history down to the stopping tolerance."""
+    from paper_1912_03106_b200 import (CycleSpec, GpuFemProblem, MgritSolver, StoppingCriterion,
+                                       TimeHierarchy, build_uniform_grid, configs)
+    spec = configs.config2(N=512, n_steps=64, levels=2, grids=1, strategy="none")
+    spec["inner"]["dt_merge_rtol"] = 1e-12
+    tf = spec["tf"] * 64 / 2 ** 14
+    hists = []
+    for on in (True, False):
+        spec["inner"]["strips"] = on
+        prob = GpuFemProblem(spec, inner="cholesky")
+        grid = build_uniform_grid(0.0, tf, 64)
+        solver = MgritSolver(prob, TimeHierarchy.build(grid, [8]),
+                             CycleSpec(kind="V", gamma=1, max_iters=10, spatial_strategy="none"),
+                             StoppingCriterion(tolerance=1e-7))
+        run, _ = solver.solve(gather_solution=False)
+        hists.append((run.iterations, np.array([run.initial_residual] + run.residual_norms)))
+        del solver
+        prob.close()
+    assert hists[0][0] == hists[1][0]
+    hs, hn = hists[0][1], hists[1][1]
+    above = hn >= 1e-7
+    assert np.max(np.abs(hs - hn)[above] / hn[above]) < 1e-8
+    assert np.max(np.abs(hs - hn)) < 1e-13 * hn[0]

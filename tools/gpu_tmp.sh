@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-PINTGPU_GRAPHS=0 timeout 1200 python tools/probe_breakdown.py cfg4 merge > gpurun_out/bd_cfg4_strips4.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_strips.py -q --durations=5 > gpurun_out/pytest_strips.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strips.log
