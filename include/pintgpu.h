@@ -227,8 +227,11 @@ typedef struct pg_kernel_profile {
  * pg_profile_read fills up to n of the PG_PROFILE_KINDS entries, in order:
  * k_sdir, k_supd (Jacobi-PCG), k_band_solve (= chains + SPIKE recombination),
  * band_chain_fwd, band_chain_bwd (column groups of 8 / 16), band_rhs,
- * spike_border, spike_fix, band_scatter, chain32_fwd, chain32_bwd (the
- * 32-column groups of GPU-filling batches, k_band_rb<32, ...>);
+ * spike_border, spike_fix (strip calls: the separator coupling + GEMM),
+ * band_scatter (strip calls: the gathers and the scatter), chain32_fwd,
+ * chain32_bwd (the chains of GPU-filling batches: k_band_rb<32, ...>, or
+ * k_band_wcol on the 8-strip systems; the 16-strip chains of smaller batches
+ * count as band_chain_*);
  * alg_flops / alg_bytes are the algorithmic work (the
  * reference's dpbtrs: 2 n w flops per direction and column). */
 #define PG_PROFILE_KINDS 11
